@@ -1,0 +1,221 @@
+/* ipm_oracle.c — the CPU ORACLE for the OpenACC `reduction(op:var)` clause.
+ *
+ * TEST INFRASTRUCTURE ONLY. Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+ * reference legs may load this library. The product path (paper_1412_1127_b200/) never does; it shares no
+ * code, header, table or constant with this file.
+ *
+ * What it computes: the plain sequential left fold that the clause denotes. The paper gives the clause
+ * only as source syntax and as a two-level scheme ("reducing along threads of thread block on GPU and
+ * reducing along thread block on CPU"; "merges results across different thread blocks",
+ * PAPER.md:106). Whatever the grouping, the result the clause defines is
+ *
+ *     var = var_original ⊕ a[0] ⊕ a[1] ⊕ ... ⊕ a[n-1]           (left fold, "folds all
+ *                                                               partials with op into the original host
+ *                                                               variable"; SPEC.md:317 identity init)
+ *
+ * and that is what is written out here, one element at a time, in index order — no blocking, no
+ * reordering. Readings where the paper is silent (DESIGN.md §"Readings"):
+ *   R1  the original var value participates; n == 0 gives var unchanged
+ *   R3  integer + and * wrap modulo 2^w (two's complement), computed in unsigned arithmetic
+ *   R5  ops + * max min & | ^ && || (BASELINE.json north_star); & | ^ are illegal on floats (C forbids
+ *       them); && || use C truthiness (x != 0: -0.0 is false, NaN is true) and produce 0/1
+ *   R6/R7 float + is accumulated in long double with Neumaier compensation (error ~2u_ld, independent of
+ *       n), float * in long double; the value reported is that long double, rounded once to T for `out`
+ *   R10 float max/min are IEEE 754-2019 maximum/minimum: -0 < +0, any NaN operand gives NaN (reported as
+ *       the canonical quiet NaN)
+ *   R2  float max/min identities are -inf / +inf
+ *
+ * Pins (tests/test_oracle.py): closed forms (Σi, n!, odd-residue products, XOR/OR of 0..n-1), brute force
+ * against Python big integers / fractions.Fraction on tiny inputs, math.fsum, numpy ufunc.reduce with the
+ * wrapping dtype, planted-extreme / planted-bit patterns, the worked examples of SPEC.md:320-322.
+ */
+#include <float.h>
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+#if LDBL_MANT_DIG < 64
+#error "the oracle needs an x87 80-bit (or wider) long double (SURVEY.md §8(c) reading 7)"
+#endif
+
+/* op / dtype numbering used by this file's own C API (the Python wrapper maps names onto these) */
+enum { O_ADD = 0, O_MUL, O_MAX, O_MIN, O_BAND, O_BOR, O_BXOR, O_LAND, O_LOR, O_NOPS };
+enum { T_I32 = 0, T_I64, T_F32, T_F64, T_NTYPES };
+
+typedef struct {
+  int32_t op, dt;
+  uint64_t r;       /* integer ops: running value (unsigned representation, w bits); logical ops: 0/1 */
+  long double s, c; /* float + : Neumaier sum and compensation; float * : s = running product */
+  double m;         /* float max/min: running value (exact copy of a T value) */
+  int64_t count;
+} ora_state;
+
+static int is_float(int dt) { return dt == T_F32 || dt == T_F64; }
+static uint64_t wmask(int dt) { return (dt == T_I32 || dt == T_F32) ? 0xFFFFFFFFull : ~0ull; }
+
+int ora_state_size(void) { return (int)sizeof(ora_state); }
+
+int ora_legal(int op, int dt) {
+  if (op < 0 || op >= O_NOPS || dt < 0 || dt >= T_NTYPES) return 0;
+  if (is_float(dt) && (op == O_BAND || op == O_BOR || op == O_BXOR)) return 0; /* C: no bitwise on floats */
+  return 1;
+}
+
+/* ---- reading one element (integers as unsigned w-bit words, floats as their value) ---- */
+static uint64_t int_at(int dt, const void* p, int64_t i) {
+  if (dt == T_I32) return (uint64_t)((const uint32_t*)p)[i];
+  return ((const uint64_t*)p)[i];
+}
+static double flt_at(int dt, const void* p, int64_t i) {
+  if (dt == T_F32) return (double)((const float*)p)[i];
+  return ((const double*)p)[i];
+}
+static int64_t as_signed(int dt, uint64_t u) { /* two's-complement reading of a w-bit word */
+  if (dt == T_I32) return (int64_t)(int32_t)(uint32_t)u;
+  return (int64_t)u;
+}
+
+/* identity of each op ("per-thread private v initialized to op's identity"; R2) */
+static void identity(int op, int dt, ora_state* st) {
+  st->r = 0; st->s = 0; st->c = 0; st->m = 0;
+  if (!is_float(dt)) {
+    switch (op) {
+      case O_ADD: case O_BOR: case O_BXOR: st->r = 0; break;
+      case O_MUL: st->r = 1; break;
+      case O_MAX: st->r = (dt == T_I32) ? 0x80000000ull : 0x8000000000000000ull; break; /* INT_MIN */
+      case O_MIN: st->r = (dt == T_I32) ? 0x7FFFFFFFull : 0x7FFFFFFFFFFFFFFFull; break; /* INT_MAX */
+      case O_BAND: st->r = wmask(dt); break;
+      case O_LAND: st->r = 1; break;
+      case O_LOR: st->r = 0; break;
+    }
+  } else {
+    switch (op) {
+      case O_ADD: st->s = 0.0L; break;
+      case O_MUL: st->s = 1.0L; break;
+      case O_MAX: st->m = -INFINITY; break;
+      case O_MIN: st->m = INFINITY; break;
+      case O_LAND: st->r = 1; break;
+      case O_LOR: st->r = 0; break;
+    }
+  }
+}
+
+/* IEEE 754-2019 maximum / minimum (R10) on two values of the same type T (exact in double) */
+static double ieee_maximum(double a, double b) {
+  if (isnan(a) || isnan(b)) return NAN;
+  if (a == 0.0 && b == 0.0) return signbit(a) ? b : a; /* -0 < +0 */
+  return (b > a) ? b : a;
+}
+static double ieee_minimum(double a, double b) {
+  if (isnan(a) || isnan(b)) return NAN;
+  if (a == 0.0 && b == 0.0) return signbit(a) ? a : b;
+  return (b < a) ? b : a;
+}
+
+/* one step of the left fold: r = r ⊕ x (x = element i of array p) */
+static void step(ora_state* st, const void* p, int64_t i) {
+  const int dt = st->dt;
+  if (!is_float(dt)) {
+    const uint64_t x = int_at(dt, p, i), M = wmask(dt);
+    switch (st->op) {
+      case O_ADD: st->r = (st->r + x) & M; break;                 /* R3: wraps mod 2^w */
+      case O_MUL: st->r = (st->r * x) & M; break;                 /* R3 */
+      case O_MAX: if (as_signed(dt, x) > as_signed(dt, st->r)) st->r = x; break;
+      case O_MIN: if (as_signed(dt, x) < as_signed(dt, st->r)) st->r = x; break;
+      case O_BAND: st->r &= x; break;
+      case O_BOR: st->r |= x; break;
+      case O_BXOR: st->r ^= x; break;
+      case O_LAND: st->r = (st->r != 0) && (x != 0); break;       /* no short circuit: every a[i] is read */
+      case O_LOR: st->r = (st->r != 0) || (x != 0); break;
+    }
+  } else {
+    const double x = flt_at(dt, p, i);
+    switch (st->op) {
+      case O_ADD: { /* Neumaier's improved Kahan–Babuška summation in long double (R7) */
+        const long double xl = (long double)x, t = st->s + xl;
+        if (fabsl(st->s) >= fabsl(xl)) st->c += (st->s - t) + xl;
+        else st->c += (xl - t) + st->s;
+        st->s = t;
+        break;
+      }
+      case O_MUL: st->s *= (long double)x; break;
+      case O_MAX: st->m = ieee_maximum(st->m, x); break;
+      case O_MIN: st->m = ieee_minimum(st->m, x); break;
+      case O_LAND: st->r = (st->r != 0) && (x != 0.0); break;     /* C truthiness: -0.0 false, NaN true */
+      case O_LOR: st->r = (st->r != 0) || (x != 0.0); break;
+    }
+  }
+  st->count++;
+}
+
+/* start the fold from the variable's original value (R1); init == NULL means the op's identity */
+int ora_begin(ora_state* st, int op, int dt, const void* init) {
+  if (!ora_legal(op, dt)) return 1;
+  memset(st, 0, sizeof *st);
+  st->op = op; st->dt = dt;
+  identity(op, dt, st);
+  if (init) {
+    /* r = identity ⊕ init == init; done through the same step so that && || normalise to 0/1 */
+    step(st, init, 0);
+    st->count = 0;
+  }
+  return 0;
+}
+
+void ora_fold(ora_state* st, const void* a, int64_t n) {
+  for (int64_t i = 0; i < n; ++i) step(st, a, i);
+}
+
+/* out: the result as a T value; out_ld: the oracle's value in long double (floats: before rounding) */
+void ora_result(const ora_state* st, void* out, long double* out_ld) {
+  const int dt = st->dt;
+  long double v;
+  if (!is_float(dt)) {
+    if (dt == T_I32) { const uint32_t w = (uint32_t)st->r; if (out) memcpy(out, &w, 4); }
+    else { if (out) memcpy(out, &st->r, 8); }
+    v = (long double)as_signed(dt, st->r);
+  } else {
+    if (st->op == O_ADD) v = st->s + st->c;
+    else if (st->op == O_MUL) v = st->s;
+    else if (st->op == O_MAX || st->op == O_MIN) v = (long double)st->m;
+    else v = (long double)(st->r ? 1 : 0);
+    if (out) {
+      if (dt == T_F32) {
+        float f = (float)v;
+        if (isnan(f)) { const uint32_t q = 0x7FC00000u; memcpy(&f, &q, 4); } /* canonical quiet NaN */
+        memcpy(out, &f, 4);
+      } else {
+        double d = (double)v;
+        if (isnan(d)) { const uint64_t q = 0x7FF8000000000000ull; memcpy(&d, &q, 8); }
+        memcpy(out, &d, 8);
+      }
+    }
+  }
+  if (out_ld) *out_ld = v;
+}
+
+/* flat clause: var = init ⊕ fold(a[0..n)) */
+int ora_reduce(int op, int dt, const void* a, int64_t n, const void* init, void* out, long double* out_ld) {
+  ora_state st;
+  if (ora_begin(&st, op, dt, init)) return 1;
+  if (n < 0) return 2;
+  ora_fold(&st, a, n);
+  ora_result(&st, out, out_ld);
+  return 0;
+}
+
+/* nested gang-outer / vector-inner clause (BASELINE.json north_star "segmented per-row reduction"):
+ * out[r] = init ⊕ fold_j a[r*stride + j], j = 0..cols-1, each row an independent fold */
+int ora_reduce_segmented(int op, int dt, const void* a, int64_t rows, int64_t cols, int64_t stride,
+                         const void* init, void* out, long double* out_ld) {
+  if (!ora_legal(op, dt)) return 1;
+  if (rows < 0 || cols < 0 || stride < cols) return 2;
+  const int es = (dt == T_I32 || dt == T_F32) ? 4 : 8;
+  for (int64_t r = 0; r < rows; ++r) {
+    ora_state st;
+    ora_begin(&st, op, dt, init);
+    ora_fold(&st, (const char*)a + (size_t)(r * stride) * es, cols);
+    ora_result(&st, out ? (char*)out + (size_t)r * es : 0, out_ld ? out_ld + r : 0);
+  }
+  return 0;
+}
