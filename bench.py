@@ -1,0 +1,409 @@
+"""bench.py — the headline benchmark: `reduction(+:sum)` sharded over 2^34 float32 (BASELINE.json config 5) on N GPUs.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--no-suite] [--no-e2e]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (one process per GPU, NCCL)
+
+One step = one execution of the clause over the whole 2^34-element iteration space: every rank runs the flat
+reduction kernel over its contiguous shard (rows a1-a6 of SURVEY.md §8(a)), one ncclAllGather exchanges the
+accumulator partials and a one-warp kernel folds them in rank order (a9), result left in device memory.
+Inputs are generated on the device (ipmgen) before timing and are larger than L2 (64/N GiB per GPU), so no
+flush is needed between steps. Timed with CUDA events between two barriers, max over ranks.
+
+Rank 0 prints ONE JSON line. Besides the contract keys it carries:
+  roofline      the flat kernel's HBM roofline: algorithmic bytes per launch / its live per-launch event time
+  cpu_baseline  the CPU oracle (test infrastructure, tests/ + here only) timed on a bounded sample, 1 core
+  e2e           the same metric through ipm_reduce_host: pinned host shard -> device inside the timed region
+  suite         (N=1) the other BASELINE configs device-timed: C1 latency, C2 per op, C3 segmented, C4 per op
+`--impl reference` times the CPU oracle as the reference arm on the same metric (no GPU work).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_TOTAL = 1 << 34          # config 5: 2^34 float32 = 64 GiB
+ELEM = 4
+METRIC = "reduction GB/s per GPU (% of B200 HBM peak) and elements/s at 1/2/4/8 GPUs"
+WORKLOAD = "C5: sharded reduction(+:sum) over 2^34 float32 (dyadic uniform [0,1024), seed 1), fp64 accumulation"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs: torch copy, read+write bytes)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+class Clocks:
+    """Sample SM clock and throttle reasons with NVML during the timed region."""
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, device_index: int):
+        self.samples, self.reasons, self.ok = [], set(), False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def harmonic(xs):
+    return len(xs) / sum(1.0 / x for x in xs) if xs and all(x > 0 for x in xs) else None
+
+
+# --------------------------------------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    """The CPU oracle as the reference arm: each step folds a bounded sample of the C5 input on 1 host core."""
+    if rank != 0:
+        return
+    import numpy as np
+
+    import ipmgen
+    import oracle
+    sample = 1 << 27  # elements per step (512 MiB of float32): about 1 s per step on one core
+    spec = ipmgen.Spec("float32", N_TOTAL, "random", seed=1)
+    a = ipmgen.fill_host(spec, 0, sample)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        oracle.reduce("+", a)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    per_step = sum(times) / len(times)
+    gbs = sample * ELEM / per_step / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "n_total": N_TOTAL, "sample_elements_per_step": sample},
+            "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": 1, "kind": "oracle",
+                             "sample": f"first 2^27 elements of the C5 input per step (host array), "
+                                       f"long double Neumaier fold; host has {host_cores()} cores"},
+            "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "elements_per_s": sample / per_step, "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+    del np
+
+
+# --------------------------------------------------------------------------------------------- our arm
+def cpu_baseline_oracle(x_dev, seconds_target=10.0):
+    """The oracle, as it stands, timed on the host over a bounded prefix of this rank's input."""
+    import numpy as np
+
+    import oracle
+    n = min(x_dev.numel(), 1 << 30)
+    a = x_dev[:n].cpu().numpy()
+    # time a small piece first to size the sample to ~seconds_target
+    t0 = time.perf_counter()
+    oracle.reduce("+", a[: 1 << 22])
+    per = (time.perf_counter() - t0) / (1 << 22)
+    m = int(min(n, max(1 << 22, seconds_target / max(per, 1e-12))))
+    t0 = time.perf_counter()
+    oracle.reduce("+", a[:m])
+    dt = time.perf_counter() - t0
+    del np
+    return {"value": m * ELEM / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "sample": f"first {m} elements of rank 0's C5 shard (host copy), long double Neumaier fold, "
+                      f"{dt:.1f} s; host has {host_cores()} cores", "elements_per_s": m / dt}
+
+
+def suite(ipm, torch, ipmgen, peak):
+    """The other BASELINE configs, device-timed with the library's per-kernel events (rank 0, N=1)."""
+    out = {}
+    ws = ipm.workspace()
+
+    def timed(fn, reps=20, flush=None):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        with ipm.KernelTimer(4 * reps) as kt:
+            for _ in range(reps):
+                if flush is not None:
+                    flush()
+                fn()
+            torch.cuda.synchronize()
+        return kt.ms
+
+    # C1: 2^20 int32 (+), L2-resident: flush L2 (write 512 MiB) before each rep; report latency
+    n = 1 << 20
+    x = torch.empty(n, dtype=torch.int32, device="cuda")
+    ipmgen.fill_tensor(ipmgen.Spec("int32", n, "iota", param=1), x)
+    scratch = torch.empty(1 << 27, dtype=torch.float32, device="cuda")
+    res = torch.empty(1, dtype=torch.int32, device="cuda")
+    ms = timed(lambda: ipm.reduce_async("+", x, out=res, ws=ws), flush=lambda: scratch.fill_(1.0))
+    ok = int(res.item()) == 524288
+    t0 = time.perf_counter()
+    for _ in range(50):
+        ipm.reduce("+", x, init=0)
+    host_us = (time.perf_counter() - t0) / 50 * 1e6
+    out["C1_int32_add_2^20"] = {"kernel_us_median": statistics.median(ms) * 1e3, "kernel_us_min": min(ms) * 1e3,
+                                "sync_call_us": host_us, "GB/s": n * 4 / statistics.median(ms) / 1e6,
+                                "closed_form_ok": ok, "note": "L2 flushed before each rep; latency-bound"}
+    del x, scratch
+    # C2: 2^28 float32 / float64, + * max min
+    for dt, tdt in (("float32", torch.float32), ("float64", torch.float64)):
+        n = 1 << 28
+        for op in ("+", "*", "max", "min"):
+            kind = {"+": "random", "*": "signs", "max": "signed", "min": "signed"}[op]
+            spec = ipmgen.Spec(dt, n, kind, seed=1, plant="factor" if op == "*" else "none",
+                               nplant=64 if op == "*" else 0)
+            x = torch.empty(n, dtype=tdt, device="cuda")
+            ipmgen.fill_tensor(spec, x)
+            r = torch.empty(1, dtype=tdt, device="cuda")
+            ms = timed(lambda: ipm.reduce_async(op, x, out=r, ws=ws))
+            med = statistics.median(ms)
+            gbs = x.numel() * x.element_size() / med / 1e6
+            out[f"C2_{dt}_{op}_2^28"] = {"kernel_ms_median": med, "GB/s": gbs, "frac": gbs / peak}
+            del x
+    # C3: 65536 x 4096 float32 row sums (segmented)
+    rows, cols = 65536, 4096
+    x = torch.empty(rows * cols, dtype=torch.float32, device="cuda")
+    ipmgen.fill_tensor(ipmgen.Spec("float32", rows * cols, "random", seed=1), x)
+    o = torch.empty(rows, dtype=torch.float32, device="cuda")
+    ms = timed(lambda: ipm.reduce_segmented("+", x.view(rows, cols), out=o, ws=ws))
+    med = statistics.median(ms)
+    gbs = (rows * cols * 4 + rows * 4) / med / 1e6
+    out["C3_float32_segmented_65536x4096"] = {"kernel_ms_median": med, "GB/s": gbs, "frac": gbs / peak}
+    del x, o
+    # C4: 2^30 int32 / int64, & | ^ && ||
+    for dt, tdt in (("int32", torch.int32), ("int64", torch.int64)):
+        n = 1 << 30
+        x = torch.empty(n, dtype=tdt, device="cuda")
+        for op in ("&", "|", "^", "&&", "||"):
+            spec = {"&": ipmgen.Spec(dt, n, "allbits", seed=1, plant="clearbit", nplant=8),
+                    "|": ipmgen.Spec(dt, n, "const", param=0, seed=1, plant="setbit", nplant=8),
+                    "^": ipmgen.Spec(dt, n, "random", seed=1),
+                    "&&": ipmgen.Spec(dt, n, "nonzero", seed=1, plant="value", nplant=1, plant_param=0),
+                    "||": ipmgen.Spec(dt, n, "const", param=0, seed=1, plant="value", nplant=1, plant_param=3)}[op]
+            ipmgen.fill_tensor(spec, x)
+            r = torch.empty(1, dtype=tdt, device="cuda")
+            ms = timed(lambda: ipm.reduce_async(op, x, out=r, ws=ws), reps=10)
+            med = statistics.median(ms)
+            gbs = x.numel() * x.element_size() / med / 1e6
+            out[f"C4_{dt}_{op}_2^30"] = {"kernel_ms_median": med, "GB/s": gbs, "frac": gbs / peak}
+        del x
+    torch.cuda.empty_cache()
+    return out
+
+
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import ipmgen
+    from paper_1412_1127_b200 import ipm
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.cuda.current_device()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        store = dist.distributed_c10d._get_default_store()
+    else:
+        store = dist.HashStore()
+    peak, peak_src = peaks()
+
+    lo, hi = ipm.shard_range(N_TOTAL, rank, world)
+    n_shard = hi - lo
+    spec = ipmgen.Spec("float32", N_TOTAL, "random", seed=1)
+    x = torch.empty(n_shard, dtype=torch.float32, device="cuda")
+    ipmgen.fill_device(spec, x.data_ptr(), lo, n_shard, torch.cuda.current_stream().cuda_stream)
+    comm = ipm.Comm(rank, world, dev, store=store)
+    ws = ipm.workspace()
+    out = torch.empty(1, dtype=torch.float32, device="cuda")
+    init = np.float32(0.0)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        comm.reduce_async("+", x, init=init, out=out, ws=ws)
+    barrier()
+
+    stream = torch.cuda.current_stream()
+    step_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(dev) as clk, ipm.KernelTimer(4 * args.steps + 8) as kt:
+        start.record(stream)
+        for i in range(args.steps):
+            step_ev[i][0].record(stream)
+            comm.reduce_async("+", x, init=init, out=out, ws=ws)
+            step_ev[i][1].record(stream)
+        stop.record(stream)
+        stop.synchronize()
+    barrier()
+    ms_local = start.elapsed_time(stop)
+    t = torch.tensor([ms_local], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    step_ms = [a.elapsed_time(b) for a, b in step_ev]
+    kern_ms = [m for m, k in zip(kt.ms, kt.kinds) if k == 0]
+    result = float(out.item())
+
+    total_bytes = N_TOTAL * ELEM
+    value = total_bytes / (ms_step / 1e3) / 1e9  # whole-job GB/s
+    kern_avg = sum(kern_ms) / len(kern_ms)
+    achieved = n_shard * ELEM / (kern_avg / 1e3) / 1e9
+
+    # e2e through the public host-array call: pinned host shard -> device each step (ipm_reduce_host)
+    e2e = None
+    if not args.no_e2e:
+        try:
+            e2e_steps = max(1, min(args.steps, 3))
+            host = torch.empty(n_shard, dtype=torch.float32, pin_memory=True)
+            host.copy_(x)
+            del x
+            torch.cuda.empty_cache()
+            for _ in range(1):
+                ipm.reduce_host("+", host, init=init, ws=ws)  # warm (allocates the staging buffers)
+            barrier()
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            t0.record(stream)
+            for _ in range(e2e_steps):
+                part = ipm.reduce_host("+", host, init=init, ws=ws)  # local shard, D2H of the result
+            t1.record(stream)
+            t1.synchronize()
+            barrier()
+            e_ms = torch.tensor([t0.elapsed_time(t1) / e2e_steps], dtype=torch.float64, device="cuda")
+            if world > 1:
+                dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+            e2e = {"value": total_bytes / (float(e_ms.item()) / 1e3) / 1e9, "unit": "GB/s",
+                   "h2d_bytes_per_step": total_bytes, "d2h_bytes_per_step": 4 * world, "steps": e2e_steps,
+                   "ms_per_step": float(e_ms.item()), "path": "ipm_reduce_host: pinned host shard, 64 MiB chunks "
+                   "double-buffered H2D overlapped with the reduce kernels", "host_result_rank0": float(part)}
+            del host
+            ipm.lib.ipm_release_staging()
+        except Exception as ex:  # pinned allocation can fail on small hosts: say so, keep the device number
+            e2e = {"value": None, "unit": "GB/s", "h2d_bytes_per_step": total_bytes, "d2h_bytes_per_step": 4 * world,
+                   "error": repr(ex)[:200]}
+    else:
+        del x
+    torch.cuda.empty_cache()
+
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu:
+            xs = torch.empty(min(n_shard, 1 << 30), dtype=torch.float32, device="cuda")
+            ipmgen.fill_device(spec, xs.data_ptr(), lo, xs.numel(), torch.cuda.current_stream().cuda_stream)
+            cpu = cpu_baseline_oracle(xs)
+            del xs
+        st = suite(ipm, torch, ipmgen, peak) if (world == 1 and not args.no_suite) else None
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "r01_traffic.json")
+        if os.path.exists(tp):
+            try:
+                tr = json.load(open(tp))
+                if int(tr.get("n_per_launch", -1)) == n_shard:
+                    traffic = tr["dram_bytes_per_launch"]
+            except Exception:
+                pass
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "input_dtype": "f32", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "n_total": N_TOTAL, "n_per_gpu": n_shard,
+                       "parallelism": f"shard{world}+ncclAllGather(8B/rank)",
+                       "l2": "inputs larger than L2 (64/N GiB per GPU): no flush needed"},
+            "per_gpu_GBs": value / world, "pct_of_hbm_peak": 100.0 * value / world / peak,
+            "elements_per_s": N_TOTAL / (ms_step / 1e3),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "kernel": "k_flat<Red<+,f32>> (one launch per step per GPU)",
+                         "bytes_per_launch": n_shard * ELEM, "kernel_ms_avg": kern_avg,
+                         "kernel_ms_min": min(kern_ms), "launches_timed": len(kern_ms),
+                         "vs_8TBs_spec": achieved / 8000.0},
+            "step_stats_ms": {"harmonic_mean": harmonic(step_ms), "median": statistics.median(step_ms),
+                              "min": min(step_ms)},
+            "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": 2 * args.steps,
+            "gpu_launches_note": "per step: 1 k_flat + 1 k_finalize (plus NCCL's own AllGather kernel)",
+            "clocks": clk.summary(), "result_rank0": result,
+        }
+        if st is not None:
+            line["suite"] = st
+        print(json.dumps(line), flush=True)
+    comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-suite", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

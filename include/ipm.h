@@ -1,0 +1,190 @@
+/* ipm.h — C ABI of libipm: B200-native execution of the OpenACC `reduction(op:var)` clause.
+ *
+ * The method (arxiv 1412.1127, IPMACC) lowers
+ *
+ *     #pragma acc loop reduction(op:var)        for (i = 0; i < n; ++i) var = var op a[i];
+ *
+ * to a kernel in which every thread folds its share of the iterations into a private copy of `var`
+ * initialised to op's identity, the copies are combined along the threads of a thread block and then
+ * across thread blocks, and the result is merged into the variable's original value
+ * (PAPER.md:97 Step 4 "iii) performing variable reductions"; PAPER.md:106 Step 7 "extra code ... that
+ * merges results across different thread blocks ... according to [Harris 2006]"; PAPER.md:205 the two-level
+ * scheme; SPEC.md:317 the per-thread private copy and the fold "into the original host variable").
+ * OpenACC's levels map to gang/worker/vector. Here: vector = a warp (warp-level reduce
+ * instructions), worker = a CTA (shared-memory combine), gang = the grid (a last-CTA finish on the GPU
+ * instead of the paper's host loop — see DESIGN.md "What differs from the paper").
+ *
+ * Data clauses (`copyin`, `create`, `present`, `copyout`, `delete`) follow PAPER.md:26/63 ("the [start:n]
+ * pair indicates that n elements should be copied from the start element") and PAPER.md:99-100 (Step 5,
+ * "host-accelerator pointer exchange, data copy in/out ... and memory allocation"); the present-table
+ * semantics and error codes follow SPEC.md:296-304 and :391 (E_SIZE, E_PRESENT).
+ *
+ * Conventions for every entry point:
+ *   - `stream` is a cudaStream_t passed as void* (NULL = the legacy default stream).
+ *   - Device pointers are CUDA device (or managed) addresses; host pointers are ordinary (pageable or
+ *     pinned) host addresses. Nothing is retained after a call returns unless stated.
+ *   - Every call returns an ipm_status; no exception or exit() crosses the ABI. IPM_E_CUDA / IPM_E_NCCL
+ *     carry the library's error string in ipm_last_error_message() (thread-local).
+ *   - The library never allocates on the reduce path; the caller owns inputs, outputs and workspaces.
+ *   - Element types: IPM_I32 = int32_t, IPM_I64 = int64_t, IPM_F32 = float, IPM_F64 = double.
+ *   - "init" is the variable's value before the loop (a host scalar of the element type); NULL means the
+ *     op's identity. The result is init ⊕ a[0] ⊕ ... ⊕ a[n-1] (reading R1).
+ *
+ * Semantics of the ops: integer + and * wrap modulo 2^w; max/min compare signed;
+ * & | ^ act on the two's-complement bits and are illegal on floats (IPM_E_REDOP); && and || use C
+ * truthiness (x != 0; for floats -0.0 is false and NaN is true) and yield 0/1 in the element type;
+ * float max/min are IEEE 754-2019 maximum/minimum (-0 < +0; any NaN gives the canonical quiet NaN);
+ * float + and * accumulate float32 inputs in float64 and round once at the end.
+ */
+#ifndef IPM_H
+#define IPM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum { IPM_ADD = 0, IPM_MUL, IPM_MAX, IPM_MIN, IPM_BAND, IPM_BOR, IPM_BXOR, IPM_LAND, IPM_LOR } ipm_op;
+typedef enum { IPM_I32 = 0, IPM_I64, IPM_F32, IPM_F64 } ipm_dtype;
+
+typedef enum {
+  IPM_OK = 0,
+  IPM_E_REDOP,     /* op illegal for the element type (& | ^ on floats), or an unknown op */
+  IPM_E_DTYPE,     /* unknown element type */
+  IPM_E_NULL,      /* a required pointer is NULL (e.g. dev == NULL with n > 0) */
+  IPM_E_SIZE,      /* negative or overflowing count, row_stride < cols, bytes == 0 for a data clause */
+  IPM_E_PRESENT,   /* `present`/`copyout`/`delete` on host memory with no live device copy */
+  IPM_E_ALIGN,     /* a device pointer not aligned to its element size */
+  IPM_E_WORKSPACE, /* workspace NULL or not aligned to 256 bytes */
+  IPM_E_CUDA,      /* a CUDA runtime error; detail in ipm_last_error_message() */
+  IPM_E_NCCL,      /* an NCCL error; detail in ipm_last_error_message() */
+  IPM_E_ARG        /* any other invalid argument (rank/world out of range, ...) */
+} ipm_status;
+
+const char* ipm_status_str(ipm_status s);
+const char* ipm_last_error_message(void);
+/* 1 if reduction(op) is legal on dtype (30 of the 36 pairs), else 0 */
+int ipm_op_legal(ipm_op op, ipm_dtype dt);
+/* element size in bytes, 0 for an unknown dtype */
+size_t ipm_dtype_size(ipm_dtype dt);
+/* library version as 10000*major + 100*minor + patch */
+int ipm_version(void);
+
+/* ------------------------------------------------------------------ device-memory allocator hook
+ * Device memory for the data clauses comes from this allocator (default: cudaMallocAsync/cudaFreeAsync on
+ * the call's stream). The Python binding installs PyTorch's caching allocator here. `ctx` is passed back
+ * untouched. Passing NULL restores the default. The structure is copied. */
+typedef struct {
+  void* (*alloc)(size_t bytes, void* stream, void* ctx);
+  void (*free)(void* p, void* stream, void* ctx);
+  void* ctx;
+} ipm_allocator;
+ipm_status ipm_set_allocator(const ipm_allocator* a);
+
+/* ------------------------------------------------------------------ data environment (present table)
+ * The table maps a host byte range [host, host+bytes) to a device buffer with a reference count, like an
+ * OpenACC runtime's present table. Lookups accept any sub-range of a live entry.
+ *   ipm_copyin : if the range is present, ++ref and return its device address; otherwise allocate `bytes`,
+ *                copy host -> device on `stream` (the call returns after the copy completed) and ref = 1.
+ *   ipm_create : like copyin but without the transfer (acc `create`).
+ *   ipm_present: *dev = device address corresponding to `host` (which may point inside an entry whose range
+ *                covers [host, host+bytes)); IPM_E_PRESENT if none. No transfer, no ref change.
+ *   ipm_update_device / ipm_update_host: copy the sub-range host <-> device (acc `update`); IPM_E_PRESENT
+ *                if absent. Synchronous with respect to the host.
+ *   ipm_copyout: copy device -> host for the entry starting at `host` (`bytes` of it), then --ref and free
+ *                at 0. ipm_delete: --ref, free at 0, no transfer.
+ *   ipm_present_count: number of live entries (for leak tests). */
+ipm_status ipm_copyin(const void* host, size_t bytes, void** dev, void* stream);
+ipm_status ipm_create(const void* host, size_t bytes, void** dev, void* stream);
+ipm_status ipm_present(const void* host, size_t bytes, void** dev);
+ipm_status ipm_update_device(const void* host, size_t bytes, void* stream);
+ipm_status ipm_update_host(void* host, size_t bytes, void* stream);
+ipm_status ipm_copyout(void* host, size_t bytes, void* stream);
+ipm_status ipm_delete(const void* host, void* stream);
+int ipm_present_count(void);
+
+/* ------------------------------------------------------------------ reductions
+ * Workspace: a device buffer of ipm_workspace_bytes() bytes, 256-byte aligned, ZEROED once before first
+ * use (ipm_workspace_init does that). It holds the per-CTA partials, the cross-CTA ticket, the result slot
+ * and the cross-rank gather slots. Every reduce leaves the ticket at zero again, so one workspace can be
+ * reused by back-to-back calls on the same stream (and inside a CUDA graph); concurrent streams need
+ * separate workspaces. */
+size_t ipm_workspace_bytes(void);
+ipm_status ipm_workspace_init(void* ws, void* stream);
+
+/* Flat clause over a[0..n): *inout = *inout ⊕ a[0] ⊕ ... ⊕ a[n-1].
+ * dev: device array of n elements of dt, aligned to the element size. inout: host scalar of dt (in: the
+ * variable's original value, out: the result). Blocks until the result is on the host (the end of an acc
+ * compute region is a synchronisation point). n == 0 is not an error: no kernel is
+ * launched and *inout becomes init ⊕ identity (= init, normalised to 0/1 for && ||). */
+ipm_status ipm_reduce(ipm_op op, ipm_dtype dt, const void* dev, int64_t n, void* inout, void* workspace,
+                      void* stream);
+
+/* Same fold, asynchronous: init (host scalar, NULL = identity) is read during the call; the result (one
+ * element of dt) is written to device memory dev_result by the kernel, in stream order. No host
+ * synchronisation; capturable in a CUDA graph. One kernel launch (none when n == 0: a 1-thread finalize
+ * kernel writes init ⊕ identity). */
+ipm_status ipm_reduce_async(ipm_op op, ipm_dtype dt, const void* dev, int64_t n, const void* init,
+                            void* dev_result, void* workspace, void* stream);
+
+/* Nested gang-outer / vector-inner clause (BASELINE.json north_star "segmented per-row reduction"):
+ *   for r in [0, rows): dev_out[r] = init ⊕ fold_{j<cols} dev[r*row_stride + j]
+ * dev: device array, row-major, row_stride >= cols elements between row starts (any alignment to the
+ * element size). init: host scalar (NULL = identity). dev_out: rows elements of dt, device. Asynchronous
+ * (stream order). workspace may be NULL unless rows < the SM count and cols is large, in which case rows
+ * are split across CTAs and a workspace (as above) is required (IPM_E_WORKSPACE otherwise). */
+ipm_status ipm_reduce_segmented(ipm_op op, ipm_dtype dt, const void* dev, int64_t rows, int64_t cols,
+                                int64_t row_stride, const void* init, void* dev_out, void* workspace,
+                                void* stream);
+
+/* End-to-end clause over a HOST array: the data clause `copyin(a[0:n])` fused with the reduction. The host
+ * array is streamed to the device in chunks through two library-owned staging buffers (allocated once
+ * through the allocator hook and kept until ipm_release_staging), each chunk's H2D copy overlapping the
+ * reduction of the previous chunk; partial results stay on the device; one 8-byte D2H at the end.
+ * Pinned host memory is fastest; pageable memory works. Blocks until *inout holds the result. */
+ipm_status ipm_reduce_host(ipm_op op, ipm_dtype dt, const void* host, int64_t n, void* inout, void* workspace,
+                           void* stream);
+ipm_status ipm_release_staging(void);
+
+/* Kernel timing (tracing): while enabled, the library records a CUDA event pair on the launch stream around
+ * each reduction kernel it launches (flat, segmented; not the one-warp finalize), up to max_records launches
+ * (later launches are not recorded). ipm_profile_read waits for the recorded events and returns the
+ * per-launch durations in milliseconds, in launch order, plus the number of recorded launches; it also
+ * returns the kernel kind of each record in `kinds` (0 flat, 1 segmented) when non-NULL. Disable frees the
+ * events. Not thread-safe with concurrent launches from other threads. */
+ipm_status ipm_profile_enable(int max_records);
+ipm_status ipm_profile_read(float* ms, int* kinds, int max, int* count);
+ipm_status ipm_profile_disable(void);
+
+/* Launch geometry the library uses for a flat reduce of n elements (for tests and the roofline report). */
+ipm_status ipm_flat_geometry(ipm_dtype dt, int64_t n, int* grid, int* block);
+
+/* ------------------------------------------------------------------ multi-GPU (one process per GPU)
+ * The iteration space is sharded contiguously: rank r owns [r*n/P, (r+1)*n/P) (floor division, 128-bit
+ * intermediate) — ipm_shard_range computes it (pure host function). Each rank reduces its shard on its GPU
+ * into an accumulator-typed partial (no host sync), ONE ncclAllGather exchanges the P partials over
+ * NVLink/NVSwitch, and every rank folds them in rank order, merges init and rounds — so every rank gets
+ * the same bits, independent of NCCL's reduction order.
+ * Bootstrap: rank 0 calls ipm_comm_unique_id, the id (ipm_comm_id_bytes() bytes) is broadcast out of band
+ * (the Python binding uses the torch.distributed store), then every rank calls ipm_comm_init. */
+typedef struct ipm_comm ipm_comm;
+size_t ipm_comm_id_bytes(void);
+ipm_status ipm_comm_unique_id(void* id_out);
+ipm_status ipm_comm_init(ipm_comm** comm, int rank, int world, const void* id, int device);
+ipm_status ipm_comm_destroy(ipm_comm* comm);
+ipm_status ipm_shard_range(int64_t n, int rank, int world, int64_t* lo, int64_t* hi);
+/* dev_shard: this rank's n_shard elements (device); inout: host scalar, the same init on every rank (in),
+ * the global result (out). Blocks until *inout is written. */
+ipm_status ipm_reduce_dist(ipm_comm* comm, ipm_op op, ipm_dtype dt, const void* dev_shard, int64_t n_shard,
+                           void* inout, void* workspace, void* stream);
+/* Asynchronous form: result written to dev_result (device, one element) in stream order. */
+ipm_status ipm_reduce_dist_async(ipm_comm* comm, ipm_op op, ipm_dtype dt, const void* dev_shard,
+                                 int64_t n_shard, const void* init, void* dev_result, void* workspace,
+                                 void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IPM_H */

@@ -1,0 +1,705 @@
+// ipm_api.cu — the C ABI of libipm (include/ipm.h): argument validation, launch geometry, dispatch of the 30
+// legal (op, dtype) kernels, the data environment (present table), and the host-streaming path.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+
+#include "ipm.h"
+#include "ipm_internal.h"
+#include "ipm_kernels.cuh"
+
+namespace ipm {
+
+// ------------------------------------------------------------------------------------------ errors
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+ipm_status cuda_fail(cudaError_t e, const char* where) {
+  set_error(std::string(where) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")");
+  return IPM_E_CUDA;
+}
+#define CK(call)                                            \
+  do {                                                      \
+    cudaError_t e_ = (call);                                \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call);     \
+  } while (0)
+
+// ------------------------------------------------------------------------------------------ device facts
+int sm_count() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (!cache[dev]) {
+    int s = 0;
+    cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = s > 0 ? s : 148;
+  }
+  return cache[dev];
+}
+
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return (v && *v) ? atoi(v) : dflt;
+}
+
+// tuning (compile-time kernel shapes, run-time grid sizing)
+constexpr int FLAT_BLOCK = 256;
+constexpr int FLAT_U = 4;  // 4 x 32 B in flight per thread
+static int flat_ctas_per_sm() {
+  static int v = std::max(1, std::min(8, env_int("IPM_CTAS_PER_SM", 4)));
+  return v;
+}
+constexpr int SEG_WARPS = 8;
+constexpr int SEG_U = 4;
+
+size_t esize(ipm_dtype dt) {
+  switch (dt) {
+    case IPM_I32: case IPM_F32: return 4;
+    case IPM_I64: case IPM_F64: return 8;
+    default: return 0;
+  }
+}
+
+ipm_status validate(ipm_op op, ipm_dtype dt) {
+  if ((int)dt < 0 || (int)dt > IPM_F64) {
+    set_error("unknown dtype");
+    return IPM_E_DTYPE;
+  }
+  if ((int)op < 0 || (int)op > IPM_LOR) {
+    set_error("unknown reduction operator");
+    return IPM_E_REDOP;
+  }
+  if ((dt == IPM_F32 || dt == IPM_F64) && (op == IPM_BAND || op == IPM_BOR || op == IPM_BXOR)) {
+    set_error("bitwise reduction operators are illegal on floating-point types");
+    return IPM_E_REDOP;
+  }
+  return IPM_OK;
+}
+
+uint64_t scalar_bits(ipm_dtype dt, const void* s) {
+  if (!s) return 0;
+  if (esize(dt) == 4) {
+    uint32_t u;
+    memcpy(&u, s, 4);
+    return u;
+  }
+  uint64_t u;
+  memcpy(&u, s, 8);
+  return u;
+}
+
+static int64_t flat_grid(ipm_dtype dt, int64_t n) {
+  const int64_t vw = 32 / (int64_t)esize(dt);
+  const int64_t tiles = (n / vw + (int64_t)FLAT_BLOCK * FLAT_U - 1) / ((int64_t)FLAT_BLOCK * FLAT_U);
+  int64_t g = std::min<int64_t>((int64_t)sm_count() * flat_ctas_per_sm(), tiles);
+  return std::max<int64_t>(1, std::min<int64_t>(g, WS_MAX_PARTIALS));
+}
+
+// ------------------------------------------------------------------------------------------ kernel timing
+struct Prof {
+  bool on = false;
+  int max = 0, used = 0;
+  cudaEvent_t* ev = nullptr;  // 2 per record
+  int* kind = nullptr;
+};
+static Prof g_prof;
+
+struct ProfScope {  // records an event pair around one kernel launch when profiling is enabled
+  int slot = -1;
+  cudaStream_t st;
+  ProfScope(cudaStream_t s, int kind) : st(s) {
+    if (g_prof.on && g_prof.used < g_prof.max) {
+      slot = g_prof.used++;
+      g_prof.kind[slot] = kind;
+      cudaEventRecord(g_prof.ev[2 * slot], st);
+    }
+  }
+  ~ProfScope() {
+    if (slot >= 0) cudaEventRecord(g_prof.ev[2 * slot + 1], st);
+  }
+};
+
+static void prof_free() {
+  for (int i = 0; i < 2 * g_prof.max; ++i) cudaEventDestroy(g_prof.ev[i]);
+  delete[] g_prof.ev;
+  delete[] g_prof.kind;
+  g_prof = Prof();
+}
+
+// ------------------------------------------------------------------------------------------ dispatch
+#define IPM_LEGAL(X)                                                                                       \
+  X(IPM_ADD, IPM_I32) X(IPM_MUL, IPM_I32) X(IPM_MAX, IPM_I32) X(IPM_MIN, IPM_I32) X(IPM_BAND, IPM_I32)     \
+  X(IPM_BOR, IPM_I32) X(IPM_BXOR, IPM_I32) X(IPM_LAND, IPM_I32) X(IPM_LOR, IPM_I32)                        \
+  X(IPM_ADD, IPM_I64) X(IPM_MUL, IPM_I64) X(IPM_MAX, IPM_I64) X(IPM_MIN, IPM_I64) X(IPM_BAND, IPM_I64)     \
+  X(IPM_BOR, IPM_I64) X(IPM_BXOR, IPM_I64) X(IPM_LAND, IPM_I64) X(IPM_LOR, IPM_I64)                        \
+  X(IPM_ADD, IPM_F32) X(IPM_MUL, IPM_F32) X(IPM_MAX, IPM_F32) X(IPM_MIN, IPM_F32) X(IPM_LAND, IPM_F32)     \
+  X(IPM_LOR, IPM_F32)                                                                                      \
+  X(IPM_ADD, IPM_F64) X(IPM_MUL, IPM_F64) X(IPM_MAX, IPM_F64) X(IPM_MIN, IPM_F64) X(IPM_LAND, IPM_F64)     \
+  X(IPM_LOR, IPM_F64)
+
+template <int OP, int DT>
+struct Launch {
+  using R = Red<OP, DT>;
+  static void flat(const FlatParams& p, dim3 grid, cudaStream_t st) {
+    k_flat<R, FLAT_BLOCK, FLAT_U><<<grid, FLAT_BLOCK, 0, st>>>(p);
+  }
+  static void seg_warp(const SegParams& p, int grid, cudaStream_t st) {
+    k_seg_warp<R, SEG_WARPS, SEG_U><<<grid, SEG_WARPS * 32, 0, st>>>(p);
+  }
+  static void seg_group(const SegParams& p, int G, int grid, cudaStream_t st) {
+    switch (G) {
+      case 1: k_seg_group<R, 1><<<grid, 256, 0, st>>>(p); break;
+      case 2: k_seg_group<R, 2><<<grid, 256, 0, st>>>(p); break;
+      case 4: k_seg_group<R, 4><<<grid, 256, 0, st>>>(p); break;
+      case 8: k_seg_group<R, 8><<<grid, 256, 0, st>>>(p); break;
+      default: k_seg_group<R, 16><<<grid, 256, 0, st>>>(p); break;
+    }
+  }
+  static void finalize(const uint64_t* slots, int P, uint64_t init, int has_init, void* out, cudaStream_t st) {
+    k_finalize<R><<<1, 32, 0, st>>>(slots, P, init, has_init, out);
+  }
+};
+
+struct Table {
+  void (*flat)(const FlatParams&, dim3, cudaStream_t);
+  void (*seg_warp)(const SegParams&, int, cudaStream_t);
+  void (*seg_group)(const SegParams&, int, int, cudaStream_t);
+  void (*finalize)(const uint64_t*, int, uint64_t, int, void*, cudaStream_t);
+};
+
+static const Table* table(ipm_op op, ipm_dtype dt) {
+#define IPM_ENTRY(O, D)                                                                                  \
+  if (op == O && dt == D) {                                                                            \
+    static const Table t = {&Launch<O, D>::flat, &Launch<O, D>::seg_warp, &Launch<O, D>::seg_group,   \
+                            &Launch<O, D>::finalize};                                                  \
+    return &t;                                                                                         \
+  }
+  IPM_LEGAL(IPM_ENTRY)
+#undef IPM_ENTRY
+  return nullptr;
+}
+
+static ipm_status check_ws(void* ws) {
+  if (!ws || ((uintptr_t)ws & 255u)) {
+    set_error("workspace must be a non-NULL, 256-byte aligned device buffer of ipm_workspace_bytes() bytes");
+    return IPM_E_WORKSPACE;
+  }
+  return IPM_OK;
+}
+
+static ipm_status check_array(ipm_dtype dt, const void* dev, int64_t n) {
+  if (n < 0) {
+    set_error("negative element count");
+    return IPM_E_SIZE;
+  }
+  if (n > 0 && !dev) {
+    set_error("NULL device array with n > 0");
+    return IPM_E_NULL;
+  }
+  if (dev && ((uintptr_t)dev % esize(dt))) {
+    set_error("device array not aligned to its element size");
+    return IPM_E_ALIGN;
+  }
+  return IPM_OK;
+}
+
+ipm_status launch_flat(ipm_op op, ipm_dtype dt, const void* dev, int64_t n, uint64_t init, int has_init, int mode,
+                       void* out, void* ws, cudaStream_t st) {
+  const Table* t = table(op, dt);
+  FlatParams p;
+  p.a = dev;
+  p.n = n;
+  p.row_stride = 0;
+  p.init = init;
+  p.has_init = has_init;
+  p.mode = mode;
+  p.out = out;
+  p.partials = (uint64_t*)((char*)ws + WS_PARTIALS);
+  p.tickets = (unsigned*)((char*)ws + WS_TICKETS);
+  {
+    ProfScope ps(st, 0);
+    t->flat(p, dim3((unsigned)flat_grid(dt, n), 1, 1), st);
+  }
+  CK(cudaGetLastError());
+  return IPM_OK;
+}
+
+ipm_status launch_finalize(ipm_op op, ipm_dtype dt, const uint64_t* slots, int P, uint64_t init, int has_init,
+                           void* out, cudaStream_t st) {
+  table(op, dt)->finalize(slots, P, init, has_init, out, st);
+  CK(cudaGetLastError());
+  return IPM_OK;
+}
+
+// ------------------------------------------------------------------------------------------ allocator
+static std::mutex g_mu;
+static ipm_allocator g_alloc = {nullptr, nullptr, nullptr};
+
+static void* dev_alloc(size_t bytes, cudaStream_t st) {
+  if (g_alloc.alloc) return g_alloc.alloc(bytes, (void*)st, g_alloc.ctx);
+  void* p = nullptr;
+  if (cudaMallocAsync(&p, bytes, st) != cudaSuccess) return nullptr;
+  return p;
+}
+static void dev_free(void* p, cudaStream_t st) {
+  if (!p) return;
+  if (g_alloc.free) g_alloc.free(p, (void*)st, g_alloc.ctx);
+  else cudaFreeAsync(p, st);
+}
+
+// ------------------------------------------------------------------------------------------ present table
+struct Entry {
+  size_t bytes;
+  void* dev;
+  int ref;
+};
+static std::map<uintptr_t, Entry> g_present;  // host start -> entry
+
+// the entry whose host range covers [h, h+bytes), or end()
+static std::map<uintptr_t, Entry>::iterator find_cover(uintptr_t h, size_t bytes) {
+  auto it = g_present.upper_bound(h);
+  if (it == g_present.begin()) return g_present.end();
+  --it;
+  if (h >= it->first && h + bytes <= it->first + it->second.bytes) return it;
+  return g_present.end();
+}
+
+// ------------------------------------------------------------------------------------------ host staging
+struct Staging {
+  void* buf[2] = {nullptr, nullptr};
+  size_t bytes = 0;
+  cudaStream_t copy = nullptr;
+  cudaEvent_t copied[2] = {nullptr, nullptr}, consumed[2] = {nullptr, nullptr};
+  int device = -1;
+};
+static Staging g_stage;
+
+static ipm_status release_staging_locked() {
+  for (int i = 0; i < 2; ++i) {
+    if (g_stage.buf[i]) {
+      cudaStreamSynchronize(g_stage.copy);
+      dev_free(g_stage.buf[i], g_stage.copy);
+      g_stage.buf[i] = nullptr;
+    }
+    if (g_stage.copied[i]) cudaEventDestroy(g_stage.copied[i]);
+    if (g_stage.consumed[i]) cudaEventDestroy(g_stage.consumed[i]);
+    g_stage.copied[i] = g_stage.consumed[i] = nullptr;
+  }
+  if (g_stage.copy) {
+    cudaStreamSynchronize(g_stage.copy);
+    cudaStreamDestroy(g_stage.copy);
+  }
+  g_stage.copy = nullptr;
+  g_stage.bytes = 0;
+  g_stage.device = -1;
+  return IPM_OK;
+}
+
+}  // namespace ipm
+
+using namespace ipm;
+
+// ============================================================================================ C ABI
+extern "C" {
+
+const char* ipm_status_str(ipm_status s) {
+  switch (s) {
+    case IPM_OK: return "IPM_OK";
+    case IPM_E_REDOP: return "IPM_E_REDOP";
+    case IPM_E_DTYPE: return "IPM_E_DTYPE";
+    case IPM_E_NULL: return "IPM_E_NULL";
+    case IPM_E_SIZE: return "IPM_E_SIZE";
+    case IPM_E_PRESENT: return "IPM_E_PRESENT";
+    case IPM_E_ALIGN: return "IPM_E_ALIGN";
+    case IPM_E_WORKSPACE: return "IPM_E_WORKSPACE";
+    case IPM_E_CUDA: return "IPM_E_CUDA";
+    case IPM_E_NCCL: return "IPM_E_NCCL";
+    case IPM_E_ARG: return "IPM_E_ARG";
+  }
+  return "IPM_E_UNKNOWN";
+}
+
+const char* ipm_last_error_message(void) { return g_err.c_str(); }
+int ipm_version(void) { return 100; }
+int ipm_op_legal(ipm_op op, ipm_dtype dt) { return validate(op, dt) == IPM_OK ? 1 : 0; }
+size_t ipm_dtype_size(ipm_dtype dt) { return esize(dt); }
+size_t ipm_workspace_bytes(void) { return WS_BYTES; }
+
+ipm_status ipm_workspace_init(void* ws, void* stream) {
+  ipm_status s = check_ws(ws);
+  if (s) return s;
+  CK(cudaMemsetAsync(ws, 0, WS_BYTES, (cudaStream_t)stream));
+  return IPM_OK;
+}
+
+ipm_status ipm_set_allocator(const ipm_allocator* a) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (a && (!a->alloc || !a->free)) {
+    set_error("allocator needs both alloc and free");
+    return IPM_E_NULL;
+  }
+  g_alloc = a ? *a : ipm_allocator{nullptr, nullptr, nullptr};
+  return IPM_OK;
+}
+
+ipm_status ipm_profile_enable(int max_records) {
+  if (max_records < 1 || max_records > (1 << 20)) {
+    set_error("max_records out of range");
+    return IPM_E_ARG;
+  }
+  prof_free();
+  g_prof.ev = new cudaEvent_t[2 * max_records];
+  g_prof.kind = new int[max_records];
+  for (int i = 0; i < 2 * max_records; ++i) {
+    cudaError_t e = cudaEventCreate(&g_prof.ev[i]);
+    if (e != cudaSuccess) {
+      g_prof.max = i / 2;
+      prof_free();
+      return cuda_fail(e, "cudaEventCreate");
+    }
+  }
+  g_prof.max = max_records;
+  g_prof.used = 0;
+  g_prof.on = true;
+  return IPM_OK;
+}
+
+ipm_status ipm_profile_read(float* ms, int* kinds, int max, int* count) {
+  if (!count) return IPM_E_NULL;
+  const int n = std::min(max, g_prof.used);
+  for (int i = 0; i < n; ++i) {
+    CK(cudaEventSynchronize(g_prof.ev[2 * i + 1]));
+    if (ms) CK(cudaEventElapsedTime(&ms[i], g_prof.ev[2 * i], g_prof.ev[2 * i + 1]));
+    if (kinds) kinds[i] = g_prof.kind[i];
+  }
+  *count = g_prof.used;
+  return IPM_OK;
+}
+
+ipm_status ipm_profile_disable(void) {
+  prof_free();
+  return IPM_OK;
+}
+
+ipm_status ipm_flat_geometry(ipm_dtype dt, int64_t n, int* grid, int* block) {
+  if (!esize(dt)) return IPM_E_DTYPE;
+  if (n < 0) return IPM_E_SIZE;
+  if (grid) *grid = (int)flat_grid(dt, n);
+  if (block) *block = FLAT_BLOCK;
+  return IPM_OK;
+}
+
+// ---------------------------------------------------------------------------------- reductions
+ipm_status ipm_reduce_async(ipm_op op, ipm_dtype dt, const void* dev, int64_t n, const void* init,
+                            void* dev_result, void* ws, void* stream) {
+  ipm_status s;
+  if ((s = validate(op, dt)) || (s = check_array(dt, dev, n)) || (s = check_ws(ws))) return s;
+  if (!dev_result) {
+    set_error("NULL dev_result");
+    return IPM_E_NULL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint64_t ib = scalar_bits(dt, init);
+  if (n == 0)  // zero-trip loop: no reduction kernel; var = init ⊕ identity
+    return launch_finalize(op, dt, nullptr, 0, ib, init != nullptr, dev_result, st);
+  return launch_flat(op, dt, dev, n, ib, init != nullptr, MODE_RESULT, dev_result, ws, st);
+}
+
+ipm_status ipm_reduce(ipm_op op, ipm_dtype dt, const void* dev, int64_t n, void* inout, void* ws, void* stream) {
+  if (!inout) {
+    set_error("NULL inout");
+    return IPM_E_NULL;
+  }
+  void* res = (char*)ws + WS_RESULT;
+  ipm_status s = ipm_reduce_async(op, dt, dev, n, inout, res, ws, stream);
+  if (s) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaMemcpyAsync(inout, res, esize(dt), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));  // end of the compute region
+  return IPM_OK;
+}
+
+ipm_status ipm_reduce_segmented(ipm_op op, ipm_dtype dt, const void* dev, int64_t rows, int64_t cols,
+                                int64_t row_stride, const void* init, void* dev_out, void* ws, void* stream) {
+  ipm_status s;
+  if ((s = validate(op, dt))) return s;
+  if (rows < 0 || cols < 0 || row_stride < cols) {
+    set_error("need rows >= 0, cols >= 0, row_stride >= cols");
+    return IPM_E_SIZE;
+  }
+  if (rows == 0) return IPM_OK;
+  if (!dev_out || (cols > 0 && !dev)) {
+    set_error("NULL device pointer");
+    return IPM_E_NULL;
+  }
+  if (((uintptr_t)dev_out % esize(dt)) || (dev && ((uintptr_t)dev % esize(dt)))) {
+    set_error("device pointer not aligned to its element size");
+    return IPM_E_ALIGN;
+  }
+  if (row_stride > 0 && (rows - 1) > (INT64_MAX - cols) / row_stride) {
+    set_error("rows*row_stride overflows");
+    return IPM_E_SIZE;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const Table* t = table(op, dt);
+  const uint64_t ib = scalar_bits(dt, init);
+  const int has_init = init != nullptr;
+  const int sms = sm_count();
+  const int64_t vw = 32 / (int64_t)esize(dt);
+
+  // few long rows: split each row over S CTAs with the flat kernel's cross-CTA finish (gridDim.y = rows)
+  const int64_t target_ctas = (int64_t)sms * flat_ctas_per_sm();
+  if (rows < 2 * (int64_t)sms && cols >= 64 * vw * FLAT_BLOCK / 8 && rows <= WS_MAX_ROWS) {
+    int64_t S = (target_ctas + rows - 1) / rows;
+    const int64_t per_cta_vecs = (cols / vw + S - 1) / S;
+    if (per_cta_vecs < FLAT_BLOCK) S = std::max<int64_t>(1, cols / vw / FLAT_BLOCK);
+    S = std::min<int64_t>(S, WS_MAX_PARTIALS / rows);
+    if (S > 1) {
+      if ((s = check_ws(ws))) return s;
+    }
+    FlatParams p;
+    p.a = dev;
+    p.n = cols;
+    p.row_stride = row_stride;
+    p.init = ib;
+    p.has_init = has_init;
+    p.mode = MODE_RESULT;
+    p.out = dev_out;
+    p.partials = ws ? (uint64_t*)((char*)ws + WS_PARTIALS) : nullptr;
+    p.tickets = ws ? (unsigned*)((char*)ws + WS_TICKETS) : nullptr;
+    {
+      ProfScope ps(st, 1);
+      t->flat(p, dim3((unsigned)S, (unsigned)rows, 1), st);
+    }
+    CK(cudaGetLastError());
+    return IPM_OK;
+  }
+  SegParams p;
+  p.a = dev;
+  p.rows = rows;
+  p.cols = cols;
+  p.row_stride = row_stride;
+  p.init = ib;
+  p.has_init = has_init;
+  p.out = dev_out;
+  ProfScope ps(st, 1);
+  if (cols >= 32) {  // one warp per row
+    const int64_t blocks = std::min<int64_t>((rows + SEG_WARPS - 1) / SEG_WARPS, (int64_t)sms * (2048 / (SEG_WARPS * 32)));
+    t->seg_warp(p, (int)std::max<int64_t>(1, blocks), st);
+  } else {           // G lanes per row, G = the power of two >= cols (capped at 16)
+    int G = 1;
+    while (G < cols && G < 16) G <<= 1;
+    const int64_t rows_per_block = 256 / G;
+    const int64_t blocks = std::min<int64_t>((rows + rows_per_block - 1) / rows_per_block, (int64_t)sms * 8);
+    t->seg_group(p, G, (int)std::max<int64_t>(1, blocks), st);
+  }
+  CK(cudaGetLastError());
+  return IPM_OK;
+}
+
+// ---------------------------------------------------------------------------------- host streaming
+ipm_status ipm_release_staging(void) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  return release_staging_locked();
+}
+
+ipm_status ipm_reduce_host(ipm_op op, ipm_dtype dt, const void* host, int64_t n, void* inout, void* ws,
+                           void* stream) {
+  ipm_status s;
+  if ((s = validate(op, dt)) || (s = check_ws(ws))) return s;
+  if (n < 0) {
+    set_error("negative element count");
+    return IPM_E_SIZE;
+  }
+  if (!inout || (n > 0 && !host)) {
+    set_error("NULL host pointer");
+    return IPM_E_NULL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t es = esize(dt);
+  const uint64_t ib = scalar_bits(dt, inout);
+  void* res = (char*)ws + WS_RESULT;
+  uint64_t* acc = (uint64_t*)((char*)ws + WS_ACC);
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (n == 0) {
+    if ((s = launch_finalize(op, dt, nullptr, 0, ib, 1, res, st))) return s;
+  } else {
+    const size_t chunk_bytes = (size_t)std::max(1, env_int("IPM_STAGE_MB", 64)) << 20;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    if (g_stage.device != dev || g_stage.bytes != chunk_bytes) {
+      release_staging_locked();
+      CK(cudaStreamCreateWithFlags(&g_stage.copy, cudaStreamNonBlocking));
+      for (int i = 0; i < 2; ++i) {
+        CK(cudaEventCreateWithFlags(&g_stage.copied[i], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&g_stage.consumed[i], cudaEventDisableTiming));
+        g_stage.buf[i] = dev_alloc(chunk_bytes, g_stage.copy);
+        if (!g_stage.buf[i]) {
+          release_staging_locked();
+          set_error("staging allocation failed");
+          return IPM_E_CUDA;
+        }
+      }
+      CK(cudaStreamSynchronize(g_stage.copy));
+      g_stage.bytes = chunk_bytes;
+      g_stage.device = dev;
+    }
+    const int64_t per = (int64_t)(chunk_bytes / es);
+    // the staging buffers are free once everything previously queued on `st` has run
+    for (int i = 0; i < 2; ++i) CK(cudaEventRecord(g_stage.consumed[i], st));
+    int64_t c = 0;
+    for (int64_t off = 0; off < n; off += per, ++c) {
+      const int b = (int)(c & 1);
+      const int64_t cnt = std::min(per, n - off);
+      CK(cudaStreamWaitEvent(g_stage.copy, g_stage.consumed[b], 0));
+      CK(cudaMemcpyAsync(g_stage.buf[b], (const char*)host + off * es, cnt * es, cudaMemcpyHostToDevice,
+                         g_stage.copy));
+      CK(cudaEventRecord(g_stage.copied[b], g_stage.copy));
+      CK(cudaStreamWaitEvent(st, g_stage.copied[b], 0));
+      if ((s = launch_flat(op, dt, g_stage.buf[b], cnt, 0, 0, c == 0 ? MODE_ACCUM_FIRST : MODE_ACCUM, acc, ws,
+                           st)))
+        return s;
+      CK(cudaEventRecord(g_stage.consumed[b], st));
+    }
+    if ((s = launch_finalize(op, dt, acc, 1, ib, 1, res, st))) return s;
+  }
+  CK(cudaMemcpyAsync(inout, res, es, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return IPM_OK;
+}
+
+// ---------------------------------------------------------------------------------- data environment
+static ipm_status present_insert(const void* host, size_t bytes, void** dev, void* stream, bool copy) {
+  if (!host || !dev) {
+    set_error("NULL pointer");
+    return IPM_E_NULL;
+  }
+  if (bytes == 0) {
+    set_error("zero-byte data clause (size unknown)");
+    return IPM_E_SIZE;
+  }
+  std::lock_guard<std::mutex> lk(g_mu);
+  const uintptr_t h = (uintptr_t)host;
+  auto it = find_cover(h, bytes);
+  if (it != g_present.end()) {  // already present: reference only (OpenACC present-or semantics)
+    it->second.ref++;
+    *dev = (char*)it->second.dev + (h - it->first);
+    return IPM_OK;
+  }
+  // a partial overlap with a live entry is an error (the OpenACC runtime forbids it)
+  auto nx = g_present.lower_bound(h);
+  if (nx != g_present.end() && nx->first < h + bytes) {
+    set_error("data clause range partially overlaps a present range");
+    return IPM_E_PRESENT;
+  }
+  if (nx != g_present.begin()) {
+    auto pv = std::prev(nx);
+    if (pv->first + pv->second.bytes > h) {
+      set_error("data clause range partially overlaps a present range");
+      return IPM_E_PRESENT;
+    }
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  void* d = dev_alloc(bytes, st);
+  if (!d) {
+    set_error("device allocation failed");
+    return IPM_E_CUDA;
+  }
+  if (copy) {
+    cudaError_t e = cudaMemcpyAsync(d, host, bytes, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+      dev_free(d, st);
+      return cuda_fail(e, "copyin");
+    }
+  }
+  g_present[h] = Entry{bytes, d, 1};
+  *dev = d;
+  return IPM_OK;
+}
+
+ipm_status ipm_copyin(const void* host, size_t bytes, void** dev, void* stream) {
+  return present_insert(host, bytes, dev, stream, true);
+}
+ipm_status ipm_create(const void* host, size_t bytes, void** dev, void* stream) {
+  return present_insert(host, bytes, dev, stream, false);
+}
+
+ipm_status ipm_present(const void* host, size_t bytes, void** dev) {
+  if (!host || !dev) {
+    set_error("NULL pointer");
+    return IPM_E_NULL;
+  }
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = find_cover((uintptr_t)host, bytes);
+  if (it == g_present.end()) {
+    set_error("no live device copy for this host range");
+    return IPM_E_PRESENT;
+  }
+  *dev = (char*)it->second.dev + ((uintptr_t)host - it->first);
+  return IPM_OK;
+}
+
+static ipm_status update(void* host, size_t bytes, void* stream, bool to_device) {
+  if (!host) {
+    set_error("NULL pointer");
+    return IPM_E_NULL;
+  }
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = find_cover((uintptr_t)host, bytes);
+  if (it == g_present.end()) {
+    set_error("no live device copy for this host range");
+    return IPM_E_PRESENT;
+  }
+  char* d = (char*)it->second.dev + ((uintptr_t)host - it->first);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (to_device) CK(cudaMemcpyAsync(d, host, bytes, cudaMemcpyHostToDevice, st));
+  else CK(cudaMemcpyAsync(host, d, bytes, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return IPM_OK;
+}
+ipm_status ipm_update_device(const void* host, size_t bytes, void* stream) {
+  return update((void*)host, bytes, stream, true);
+}
+ipm_status ipm_update_host(void* host, size_t bytes, void* stream) { return update(host, bytes, stream, false); }
+
+static ipm_status release(const void* host, size_t bytes, void* stream, bool copy) {
+  if (!host) {
+    set_error("NULL pointer");
+    return IPM_E_NULL;
+  }
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_present.find((uintptr_t)host);
+  if (it == g_present.end()) {
+    set_error("no live device copy starting at this host address");
+    return IPM_E_PRESENT;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (copy) {
+    if (bytes > it->second.bytes) {
+      set_error("copyout larger than the present range");
+      return IPM_E_SIZE;
+    }
+    CK(cudaMemcpyAsync((void*)host, it->second.dev, bytes, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  if (--it->second.ref == 0) {
+    dev_free(it->second.dev, st);
+    g_present.erase(it);
+  }
+  return IPM_OK;
+}
+ipm_status ipm_copyout(void* host, size_t bytes, void* stream) { return release(host, bytes, stream, true); }
+ipm_status ipm_delete(const void* host, void* stream) { return release(host, 0, stream, false); }
+
+int ipm_present_count(void) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  return (int)g_present.size();
+}
+
+}  // extern "C"

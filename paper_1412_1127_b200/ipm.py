@@ -1,0 +1,406 @@
+"""Python binding of libipm (include/ipm.h): argument marshalling only — every step of the reduction runs in
+the CUDA kernels of ``csrc/``. PyTorch supplies device memory (its caching allocator is installed as the
+library's allocator hook), streams and process groups.
+
+There is no fallback: if ``libipm.so`` is missing or fails to load, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libipm.so")
+
+# operator names follow the clause syntax `reduction(op:var)` (OpenACC; SPEC.md:110 plus the BASELINE.json ops)
+OPS = {"+": 0, "*": 1, "max": 2, "min": 3, "&": 4, "|": 5, "^": 6, "&&": 7, "||": 8}
+DTYPES = {torch.int32: 0, torch.int64: 1, torch.float32: 2, torch.float64: 3}
+NP_OF = {0: np.int32, 1: np.int64, 2: np.float32, 3: np.float64}
+TORCH_OF = {0: torch.int32, 1: torch.int64, 2: torch.float32, 3: torch.float64}
+STATUS = ["IPM_OK", "IPM_E_REDOP", "IPM_E_DTYPE", "IPM_E_NULL", "IPM_E_SIZE", "IPM_E_PRESENT", "IPM_E_ALIGN",
+          "IPM_E_WORKSPACE", "IPM_E_CUDA", "IPM_E_NCCL", "IPM_E_ARG"]
+
+
+class IpmError(RuntimeError):
+    def __init__(self, code: int, where: str, detail: str):
+        self.code = code
+        self.status = STATUS[code] if 0 <= code < len(STATUS) else f"status {code}"
+        super().__init__(f"{where}: {self.status}: {detail}")
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing — build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+                          " (there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i64, ci, sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_size_t
+    sigs = {
+        "ipm_status_str": ([ci], ctypes.c_char_p),
+        "ipm_last_error_message": ([], ctypes.c_char_p),
+        "ipm_op_legal": ([ci, ci], ci),
+        "ipm_dtype_size": ([ci], sz),
+        "ipm_version": ([], ci),
+        "ipm_set_allocator": ([vp], ci),
+        "ipm_copyin": ([vp, sz, ctypes.POINTER(vp), vp], ci),
+        "ipm_create": ([vp, sz, ctypes.POINTER(vp), vp], ci),
+        "ipm_present": ([vp, sz, ctypes.POINTER(vp)], ci),
+        "ipm_update_device": ([vp, sz, vp], ci),
+        "ipm_update_host": ([vp, sz, vp], ci),
+        "ipm_copyout": ([vp, sz, vp], ci),
+        "ipm_delete": ([vp, vp], ci),
+        "ipm_present_count": ([], ci),
+        "ipm_workspace_bytes": ([], sz),
+        "ipm_workspace_init": ([vp, vp], ci),
+        "ipm_reduce": ([ci, ci, vp, i64, vp, vp, vp], ci),
+        "ipm_reduce_async": ([ci, ci, vp, i64, vp, vp, vp, vp], ci),
+        "ipm_reduce_segmented": ([ci, ci, vp, i64, i64, i64, vp, vp, vp, vp], ci),
+        "ipm_reduce_host": ([ci, ci, vp, i64, vp, vp, vp], ci),
+        "ipm_release_staging": ([], ci),
+        "ipm_profile_enable": ([ci], ci),
+        "ipm_profile_read": ([vp, vp, ci, ctypes.POINTER(ci)], ci),
+        "ipm_profile_disable": ([], ci),
+        "ipm_flat_geometry": ([ci, i64, ctypes.POINTER(ci), ctypes.POINTER(ci)], ci),
+        "ipm_comm_id_bytes": ([], sz),
+        "ipm_comm_unique_id": ([vp], ci),
+        "ipm_comm_init": ([ctypes.POINTER(vp), ci, ci, vp, ci], ci),
+        "ipm_comm_destroy": ([vp], ci),
+        "ipm_shard_range": ([i64, ci, ci, ctypes.POINTER(i64), ctypes.POINTER(i64)], ci),
+        "ipm_reduce_dist": ([vp, ci, ci, vp, i64, vp, vp, vp], ci),
+        "ipm_reduce_dist_async": ([vp, ci, ci, vp, i64, vp, vp, vp, vp], ci),
+    }
+    for name, (args, res) in sigs.items():
+        f = getattr(L, name)  # AttributeError if the library does not export it: fail loudly
+        f.argtypes = args
+        f.restype = res
+    return L
+
+
+lib = _load()
+EXPORTED = ("ipm_status_str ipm_last_error_message ipm_op_legal ipm_dtype_size ipm_version ipm_set_allocator "
+            "ipm_copyin ipm_create ipm_present ipm_update_device ipm_update_host ipm_copyout ipm_delete "
+            "ipm_present_count ipm_workspace_bytes ipm_workspace_init ipm_reduce ipm_reduce_async "
+            "ipm_reduce_segmented ipm_reduce_host ipm_release_staging ipm_profile_enable ipm_profile_read "
+            "ipm_profile_disable ipm_flat_geometry ipm_comm_id_bytes "
+            "ipm_comm_unique_id ipm_comm_init ipm_comm_destroy ipm_shard_range ipm_reduce_dist "
+            "ipm_reduce_dist_async").split()
+
+
+def _check(code: int, where: str):
+    if code != 0:
+        raise IpmError(code, where, lib.ipm_last_error_message().decode(errors="replace"))
+
+
+# ------------------------------------------------------------------ allocator hook: PyTorch's caching allocator
+_ALLOC_T = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
+_FREE_T = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
+
+
+class _CAllocator(ctypes.Structure):
+    _fields_ = [("alloc", _ALLOC_T), ("free", _FREE_T), ("ctx", ctypes.c_void_p)]
+
+
+def _torch_alloc(nbytes, stream, ctx):
+    try:
+        return torch.cuda.caching_allocator_alloc(int(nbytes), torch.cuda.current_device(), stream or 0)
+    except Exception:  # out of memory -> NULL -> IPM_E_CUDA on the C side
+        return None
+
+
+def _torch_free(p, stream, ctx):
+    torch.cuda.caching_allocator_delete(p)
+
+
+_alloc_cb = _ALLOC_T(_torch_alloc)
+_free_cb = _FREE_T(_torch_free)
+_allocator = _CAllocator(_alloc_cb, _free_cb, None)
+_check(lib.ipm_set_allocator(ctypes.byref(_allocator)), "ipm_set_allocator")
+
+
+# ------------------------------------------------------------------ helpers
+def op_code(op: str) -> int:
+    try:
+        return OPS[op]
+    except KeyError:
+        raise ValueError(f"unknown reduction operator {op!r}; one of {list(OPS)}") from None
+
+
+def dtype_code(dt) -> int:
+    if isinstance(dt, torch.dtype):
+        return DTYPES[dt]
+    return DTYPES[{np.int32: torch.int32, np.int64: torch.int64, np.float32: torch.float32,
+                   np.float64: torch.float64}[np.dtype(dt).type]]
+
+
+def legal(op: str, dtype) -> bool:
+    return bool(lib.ipm_op_legal(op_code(op), dtype_code(dtype)))
+
+
+def _stream(stream=None) -> int:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _scalar(dt: int, value):
+    """a 1-element numpy buffer holding `value` in element type dt (None -> None)"""
+    if value is None:
+        return None
+    return np.array([value], dtype=NP_OF[dt])
+
+
+WS_BYTES = lib.ipm_workspace_bytes()
+_ws_cache: dict = {}
+_ws_lock = threading.Lock()
+
+
+def workspace(stream=None, device=None) -> torch.Tensor:
+    """The per-(device, stream) zero-initialised workspace used when none is passed explicitly."""
+    dev = torch.cuda.current_device() if device is None else device
+    s = _stream(stream)
+    with _ws_lock:
+        ws = _ws_cache.get((dev, s))
+        if ws is None:
+            ws = torch.zeros(WS_BYTES, dtype=torch.uint8, device=f"cuda:{dev}")
+            _ws_cache[(dev, s)] = ws
+    return ws
+
+
+def _flat_arg(t: torch.Tensor):
+    if not t.is_cuda:
+        raise ValueError("expected a CUDA tensor (use reduce_host for host arrays)")
+    if not t.is_contiguous():
+        raise ValueError("expected a contiguous tensor")
+    return t.data_ptr(), t.numel(), DTYPES[t.dtype]
+
+
+# ------------------------------------------------------------------ reductions
+def reduce(op: str, t: torch.Tensor, init=None, ws: torch.Tensor | None = None, stream=None):
+    """`reduction(op:var)` over all elements of a CUDA tensor; returns init ⊕ fold as a numpy scalar.
+    Blocks until the result is on the host (ipm_reduce)."""
+    ptr, n, dt = _flat_arg(t)
+    s = _stream(stream)
+    ws = workspace(stream) if ws is None else ws
+    box = _scalar(dt, init)
+    if box is None:  # no original value: start from the identity (the async path does that on device)
+        return reduce_async(op, t, None, ws=ws, stream=stream).cpu().numpy()[0]
+    _check(lib.ipm_reduce(op_code(op), dt, ptr, n, box.ctypes.data, ws.data_ptr(), s), "ipm_reduce")
+    return box[0]
+
+
+def reduce_async(op: str, t: torch.Tensor, init=None, out: torch.Tensor | None = None,
+                 ws: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Asynchronous form: returns (or fills) a 1-element CUDA tensor written in stream order."""
+    ptr, n, dt = _flat_arg(t)
+    if out is None:
+        out = torch.empty(1, dtype=t.dtype, device=t.device)
+    ws = workspace(stream) if ws is None else ws
+    box = _scalar(dt, init)
+    _check(lib.ipm_reduce_async(op_code(op), dt, ptr, n, None if box is None else box.ctypes.data, out.data_ptr(),
+                                ws.data_ptr(), _stream(stream)), "ipm_reduce_async")
+    return out
+
+
+def reduce_segmented(op: str, t: torch.Tensor, rows: int | None = None, cols: int | None = None,
+                     row_stride: int | None = None, init=None, out: torch.Tensor | None = None,
+                     ws: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Nested gang-outer / vector-inner clause: out[r] = init ⊕ fold_j t[r*row_stride + j], j < cols.
+    With a 2-D tensor, rows/cols/row_stride default to its shape and row stride."""
+    if not t.is_cuda:
+        raise ValueError("expected a CUDA tensor")
+    dt = DTYPES[t.dtype]
+    if t.dim() == 2 and rows is None:
+        rows, cols = t.shape
+        row_stride = t.stride(0)
+        if t.stride(1) != 1:
+            raise ValueError("rows must be contiguous")
+    elif rows is None or cols is None:
+        raise ValueError("rows and cols are required for a flat tensor")
+    row_stride = cols if row_stride is None else row_stride
+    if out is None:
+        out = torch.empty(rows, dtype=t.dtype, device=t.device)
+    ws = workspace(stream) if ws is None else ws
+    box = _scalar(dt, init)
+    _check(lib.ipm_reduce_segmented(op_code(op), dt, t.data_ptr(), rows, cols, row_stride,
+                                    None if box is None else box.ctypes.data, out.data_ptr(), ws.data_ptr(),
+                                    _stream(stream)), "ipm_reduce_segmented")
+    return out
+
+
+def reduce_host(op: str, a, init=None, ws: torch.Tensor | None = None, stream=None):
+    """End-to-end clause over a HOST array (numpy array or CPU tensor, pinned is fastest): copyin fused with
+    the reduction, chunked H2D overlapped with the kernels; returns the result as a numpy scalar."""
+    if isinstance(a, torch.Tensor):
+        if a.is_cuda:
+            raise ValueError("reduce_host takes a host array")
+        a = a.contiguous()
+        ptr, n, dt = a.data_ptr(), a.numel(), DTYPES[a.dtype]
+        keep = a
+    else:
+        keep = np.ascontiguousarray(a)
+        ptr, n, dt = keep.ctypes.data, keep.size, dtype_code(keep.dtype)
+    ws = workspace(stream) if ws is None else ws
+    box = _scalar(dt, init)
+    if box is None:
+        box = _scalar(dt, identity_value(op, dt))
+    _check(lib.ipm_reduce_host(op_code(op), dt, ptr, n, box.ctypes.data, ws.data_ptr(), _stream(stream)),
+           "ipm_reduce_host")
+    del keep
+    return box[0]
+
+
+def identity_value(op: str, dt: int):
+    """The identity of op on element type dt, as the library's own finalize kernel produces it (n = 0)."""
+    out = reduce_async(op, torch.empty(0, dtype=TORCH_OF[dt], device="cuda"))
+    return out.cpu().numpy()[0]
+
+
+def flat_geometry(dtype, n: int):
+    g, b = ctypes.c_int(), ctypes.c_int()
+    _check(lib.ipm_flat_geometry(dtype_code(dtype), n, ctypes.byref(g), ctypes.byref(b)), "ipm_flat_geometry")
+    return g.value, b.value
+
+
+class KernelTimer:
+    """Per-launch device time of the library's reduction kernels (CUDA events recorded by libipm on the
+    launch stream around each kernel): ``with KernelTimer(1000) as kt: ...; kt.ms -> list of floats``."""
+
+    def __init__(self, max_records: int = 4096):
+        self.max_records = max_records
+        self.ms: list[float] = []
+        self.kinds: list[int] = []
+
+    def __enter__(self):
+        _check(lib.ipm_profile_enable(self.max_records), "ipm_profile_enable")
+        return self
+
+    def read(self):
+        ms = np.zeros(self.max_records, np.float32)
+        kinds = np.zeros(self.max_records, np.int32)
+        cnt = ctypes.c_int()
+        _check(lib.ipm_profile_read(ms.ctypes.data, kinds.ctypes.data, self.max_records, ctypes.byref(cnt)),
+               "ipm_profile_read")
+        n = min(cnt.value, self.max_records)
+        self.ms, self.kinds = [float(x) for x in ms[:n]], [int(k) for k in kinds[:n]]
+        return self.ms
+
+    def __exit__(self, *exc):
+        try:
+            self.read()
+        finally:
+            lib.ipm_profile_disable()
+        return False
+
+
+# ------------------------------------------------------------------ data environment
+def copyin(host: np.ndarray, stream=None) -> int:
+    """acc `copyin(host[0:n])`: returns the device address (present-or semantics)."""
+    d = ctypes.c_void_p()
+    _check(lib.ipm_copyin(host.ctypes.data, host.nbytes, ctypes.byref(d), _stream(stream)), "ipm_copyin")
+    return d.value
+
+
+def create(host: np.ndarray, stream=None) -> int:
+    d = ctypes.c_void_p()
+    _check(lib.ipm_create(host.ctypes.data, host.nbytes, ctypes.byref(d), _stream(stream)), "ipm_create")
+    return d.value
+
+
+def present(host: np.ndarray) -> int:
+    d = ctypes.c_void_p()
+    _check(lib.ipm_present(host.ctypes.data, host.nbytes, ctypes.byref(d)), "ipm_present")
+    return d.value
+
+
+def update_device(host: np.ndarray, stream=None):
+    _check(lib.ipm_update_device(host.ctypes.data, host.nbytes, _stream(stream)), "ipm_update_device")
+
+
+def update_host(host: np.ndarray, stream=None):
+    _check(lib.ipm_update_host(host.ctypes.data, host.nbytes, _stream(stream)), "ipm_update_host")
+
+
+def copyout(host: np.ndarray, stream=None):
+    _check(lib.ipm_copyout(host.ctypes.data, host.nbytes, _stream(stream)), "ipm_copyout")
+
+
+def delete(host: np.ndarray, stream=None):
+    _check(lib.ipm_delete(host.ctypes.data, _stream(stream)), "ipm_delete")
+
+
+def present_count() -> int:
+    return lib.ipm_present_count()
+
+
+def as_tensor(dev_ptr: int, n: int, dtype: torch.dtype) -> torch.Tensor:
+    """View a device address from the present table as a CUDA tensor (no copy, not owning)."""
+    class _Holder:
+        __cuda_array_interface__ = {"shape": (n,), "typestr": np.dtype(NP_OF[DTYPES[dtype]]).str,
+                                    "data": (dev_ptr, False), "version": 3}
+    return torch.as_tensor(_Holder(), device="cuda")
+
+
+# ------------------------------------------------------------------ multi-GPU
+def shard_range(n: int, rank: int, world: int):
+    lo, hi = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib.ipm_shard_range(n, rank, world, ctypes.byref(lo), ctypes.byref(hi)), "ipm_shard_range")
+    return lo.value, hi.value
+
+
+class Comm:
+    """One NCCL communicator per process/GPU, bootstrapped through the torch.distributed store."""
+
+    def __init__(self, rank: int, world: int, device: int, store=None, key: str = "ipm_nccl_id"):
+        nb = lib.ipm_comm_id_bytes()
+        if store is None:
+            import torch.distributed as dist
+            store = dist.distributed_c10d._get_default_store()
+        if rank == 0:
+            buf = ctypes.create_string_buffer(nb)
+            _check(lib.ipm_comm_unique_id(buf), "ipm_comm_unique_id")
+            store.set(key, bytes(buf.raw))
+        uid = store.get(key)
+        if len(uid) != nb:
+            raise IpmError(10, "Comm", "bad NCCL id from store")
+        self._id = ctypes.create_string_buffer(uid, nb)
+        self._h = ctypes.c_void_p()
+        torch.cuda.set_device(device)
+        _check(lib.ipm_comm_init(ctypes.byref(self._h), rank, world, self._id, device), "ipm_comm_init")
+        self.rank, self.world, self.device = rank, world, device
+
+    def close(self):
+        if self._h:
+            _check(lib.ipm_comm_destroy(self._h), "ipm_comm_destroy")
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def reduce(self, op: str, shard: torch.Tensor, init=None, ws: torch.Tensor | None = None, stream=None):
+        """Every rank passes its shard and the same init; every rank returns the global result."""
+        ptr, n, dt = _flat_arg(shard)
+        ws = workspace(stream) if ws is None else ws
+        box = _scalar(dt, init)
+        if box is None:
+            out = self.reduce_async(op, shard, None, ws=ws, stream=stream)
+            return out.cpu().numpy()[0]
+        _check(lib.ipm_reduce_dist(self._h, op_code(op), dt, ptr, n, box.ctypes.data, ws.data_ptr(),
+                                   _stream(stream)), "ipm_reduce_dist")
+        return box[0]
+
+    def reduce_async(self, op: str, shard: torch.Tensor, init=None, out: torch.Tensor | None = None,
+                     ws: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        ptr, n, dt = _flat_arg(shard)
+        if out is None:
+            out = torch.empty(1, dtype=shard.dtype, device=shard.device)
+        ws = workspace(stream) if ws is None else ws
+        box = _scalar(dt, init)
+        _check(lib.ipm_reduce_dist_async(self._h, op_code(op), dt, ptr, n, None if box is None else box.ctypes.data,
+                                         out.data_ptr(), ws.data_ptr(), _stream(stream)), "ipm_reduce_dist_async")
+        return out
