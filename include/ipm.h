@@ -158,6 +158,14 @@ ipm_status ipm_profile_enable(int max_records);
 ipm_status ipm_profile_read(float* ms, int* kinds, int max, int* count);
 ipm_status ipm_profile_disable(void);
 
+/* Tuning options (process-wide; the defaults are the measured best):
+ *   IPM_OPT_FLAT_CTAS_PER_SM  CTAs per SM of the flat kernel's persistent grid, 1..8 (-1 = default 4)
+ *   IPM_OPT_SEG_KERNEL        segmented rows: 0 auto (direct 256-bit loads), 1 direct loads, 2 TMA bulk copies
+ *                             into a per-warp shared-memory ring (rows of >= 64 bytes)
+ * IPM_E_ARG for an unknown key or an out-of-range value. */
+typedef enum { IPM_OPT_FLAT_CTAS_PER_SM = 0, IPM_OPT_SEG_KERNEL = 1 } ipm_option;
+ipm_status ipm_set_option(ipm_option key, int64_t value);
+
 /* Launch geometry the library uses for a flat reduce of n elements (for tests and the roofline report). */
 ipm_status ipm_flat_geometry(ipm_dtype dt, int64_t n, int* grid, int* block);
 

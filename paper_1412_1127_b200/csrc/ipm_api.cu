@@ -50,12 +50,17 @@ static int env_int(const char* name, int dflt) {
 // tuning (compile-time kernel shapes, run-time grid sizing)
 constexpr int FLAT_BLOCK = 256;
 constexpr int FLAT_U = 4;  // 4 x 32 B in flight per thread
+// run-time options (ipm_set_option); defaults chosen by tools/sweep_flat.cu measurements
+static int g_opt_flat_cps = -1;  // CTAs per SM for k_flat (-1: IPM_CTAS_PER_SM env or 4)
+static int g_opt_seg_kernel = 0; // 0 auto, 1 k_seg_warp (LDG), 2 k_seg_tma (bulk copies)
 static int flat_ctas_per_sm() {
+  if (g_opt_flat_cps > 0) return g_opt_flat_cps;
   static int v = std::max(1, std::min(8, env_int("IPM_CTAS_PER_SM", 4)));
   return v;
 }
 constexpr int SEG_WARPS = 8;
-constexpr int SEG_U = 4;
+constexpr int SEG_U = 8;
+constexpr int TMA_WARPS = 8, TMA_S = 4, TMA_CH = 4096;
 
 size_t esize(ipm_dtype dt) {
   switch (dt) {
@@ -151,6 +156,14 @@ struct Launch {
   static void seg_warp(const SegParams& p, int grid, cudaStream_t st) {
     k_seg_warp<R, SEG_WARPS, SEG_U><<<grid, SEG_WARPS * 32, 0, st>>>(p);
   }
+  static cudaError_t seg_tma(const SegParams& p, int grid, cudaStream_t st) {
+    constexpr int smem = SegTma<R, TMA_WARPS, TMA_S, TMA_CH>::SMEM;
+    static cudaError_t attr =
+        cudaFuncSetAttribute(k_seg_tma<R, TMA_WARPS, TMA_S, TMA_CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (attr != cudaSuccess) return attr;
+    k_seg_tma<R, TMA_WARPS, TMA_S, TMA_CH><<<grid, TMA_WARPS * 32, smem, st>>>(p);
+    return cudaSuccess;
+  }
   static void seg_group(const SegParams& p, int G, int grid, cudaStream_t st) {
     switch (G) {
       case 1: k_seg_group<R, 1><<<grid, 256, 0, st>>>(p); break;
@@ -168,6 +181,7 @@ struct Launch {
 struct Table {
   void (*flat)(const FlatParams&, dim3, cudaStream_t);
   void (*seg_warp)(const SegParams&, int, cudaStream_t);
+  cudaError_t (*seg_tma)(const SegParams&, int, cudaStream_t);
   void (*seg_group)(const SegParams&, int, int, cudaStream_t);
   void (*finalize)(const uint64_t*, int, uint64_t, int, void*, cudaStream_t);
 };
@@ -175,8 +189,8 @@ struct Table {
 static const Table* table(ipm_op op, ipm_dtype dt) {
 #define IPM_ENTRY(O, D)                                                                                  \
   if (op == O && dt == D) {                                                                            \
-    static const Table t = {&Launch<O, D>::flat, &Launch<O, D>::seg_warp, &Launch<O, D>::seg_group,   \
-                            &Launch<O, D>::finalize};                                                  \
+    static const Table t = {&Launch<O, D>::flat, &Launch<O, D>::seg_warp, &Launch<O, D>::seg_tma,     \
+                            &Launch<O, D>::seg_group, &Launch<O, D>::finalize};                        \
     return &t;                                                                                         \
   }
   IPM_LEGAL(IPM_ENTRY)
@@ -347,6 +361,21 @@ ipm_status ipm_set_allocator(const ipm_allocator* a) {
   return IPM_OK;
 }
 
+ipm_status ipm_set_option(ipm_option key, int64_t value) {
+  switch (key) {
+    case IPM_OPT_FLAT_CTAS_PER_SM:
+      if (value < -1 || value > 8 || value == 0) break;
+      g_opt_flat_cps = (int)value;
+      return IPM_OK;
+    case IPM_OPT_SEG_KERNEL:
+      if (value < 0 || value > 2) break;
+      g_opt_seg_kernel = (int)value;
+      return IPM_OK;
+  }
+  set_error("unknown option or value out of range");
+  return IPM_E_ARG;
+}
+
 ipm_status ipm_profile_enable(int max_records) {
   if (max_records < 1 || max_records > (1 << 20)) {
     set_error("max_records out of range");
@@ -488,8 +517,12 @@ ipm_status ipm_reduce_segmented(ipm_op op, ipm_dtype dt, const void* dev, int64_
   p.has_init = has_init;
   p.out = dev_out;
   ProfScope ps(st, 1);
-  if (cols >= 32) {  // one warp per row
-    const int64_t blocks = std::min<int64_t>((rows + SEG_WARPS - 1) / SEG_WARPS, (int64_t)sms * (2048 / (SEG_WARPS * 32)));
+  const bool tma = g_opt_seg_kernel == 2 && cols * (int64_t)esize(dt) >= 64;
+  if (tma) {         // one warp per row, rows staged by TMA bulk copies (one 128 KiB-ring CTA per SM)
+    const int64_t blocks = std::min<int64_t>((rows + TMA_WARPS - 1) / TMA_WARPS, (int64_t)sms);
+    CK(t->seg_tma(p, (int)std::max<int64_t>(1, blocks), st));
+  } else if (cols >= 32) {  // one warp per row, direct 256-bit loads
+    const int64_t blocks = std::min<int64_t>((rows + SEG_WARPS - 1) / SEG_WARPS, (int64_t)sms * 4);
     t->seg_warp(p, (int)std::max<int64_t>(1, blocks), st);
   } else {           // G lanes per row, G = the power of two >= cols (capped at 16)
     int G = 1;

@@ -10,6 +10,7 @@
 //                  results across different thread blocks"; PAPER.md:205 does this on the host — see
 //                  DESIGN.md "What differs from the paper")
 //   k_seg_warp  the nested gang-outer / vector-inner clause, one warp per row (a8)
+//   k_seg_tma   the same with each row staged into shared memory by TMA bulk copies (per-warp ring)
 //   k_seg_group the same for short rows: a group of G <= 32 lanes per row
 //   k_finalize  fold of P accumulator slots (cross-rank, or cross-chunk) + init, rounding to T (a6/a9)
 #pragma once
@@ -39,21 +40,36 @@ struct Vec<uint64_t> {
   static constexpr int W = 4;
 };
 
+// HINT selects the cache policy (tools/sweep_flat.cu measures them; the product uses 0):
+//   0 ld.global.nc.L1::no_allocate.L2::evict_first.L2::256B   1 ld.global.nc.L1::no_allocate
+//   2 ld.global (plain)                                         3 ld.global.nc.L1::no_allocate.L2::256B
+#define IPM_LDV8(Q)                                                                                   \
+  asm(Q ".v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"                                                   \
+      : "=r"(v.w[0]), "=r"(v.w[1]), "=r"(v.w[2]), "=r"(v.w[3]), "=r"(v.w[4]), "=r"(v.w[5]), "=r"(v.w[6]), \
+        "=r"(v.w[7])                                                                                  \
+      : "l"(p))
+#define IPM_LDV4(Q) \
+  asm(Q ".v4.b64 {%0,%1,%2,%3}, [%4];" : "=l"(v.w[0]), "=l"(v.w[1]), "=l"(v.w[2]), "=l"(v.w[3]) : "l"(p))
+template <int HINT = 0>
 __device__ __forceinline__ V8 ldv(const V8* p) {
   V8 v;
-  asm("ld.global.nc.L1::no_allocate.L2::evict_first.L2::256B.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-      : "=r"(v.w[0]), "=r"(v.w[1]), "=r"(v.w[2]), "=r"(v.w[3]), "=r"(v.w[4]), "=r"(v.w[5]), "=r"(v.w[6]),
-        "=r"(v.w[7])
-      : "l"(p));
+  if (HINT == 0) IPM_LDV8("ld.global.nc.L1::no_allocate.L2::evict_first.L2::256B");
+  else if (HINT == 1) IPM_LDV8("ld.global.nc.L1::no_allocate");
+  else if (HINT == 2) IPM_LDV8("ld.global");
+  else IPM_LDV8("ld.global.nc.L1::no_allocate.L2::256B");
   return v;
 }
+template <int HINT = 0>
 __device__ __forceinline__ V4 ldv(const V4* p) {
   V4 v;
-  asm("ld.global.nc.L1::no_allocate.L2::evict_first.L2::256B.v4.b64 {%0,%1,%2,%3}, [%4];"
-      : "=l"(v.w[0]), "=l"(v.w[1]), "=l"(v.w[2]), "=l"(v.w[3])
-      : "l"(p));
+  if (HINT == 0) IPM_LDV4("ld.global.nc.L1::no_allocate.L2::evict_first.L2::256B");
+  else if (HINT == 1) IPM_LDV4("ld.global.nc.L1::no_allocate");
+  else if (HINT == 2) IPM_LDV4("ld.global");
+  else IPM_LDV4("ld.global.nc.L1::no_allocate.L2::256B");
   return v;
 }
+#undef IPM_LDV8
+#undef IPM_LDV4
 __device__ __forceinline__ uint32_t lds(const uint32_t* p) { return __ldg(p); }
 __device__ __forceinline__ uint64_t lds(const uint64_t* p) { return (uint64_t)__ldg((const unsigned long long*)p); }
 
@@ -108,7 +124,7 @@ __device__ __forceinline__ typename R::A block_reduce(typename R::A v, typename 
 }
 
 // ------------------------------------------------------------------------------------------ flat
-template <class R, int BLOCK, int U>
+template <class R, int BLOCK, int U, int HINT = 0>
 __global__ void __launch_bounds__(BLOCK) k_flat(FlatParams p) {
   using B = typename R::B;
   using A = typename R::A;
@@ -139,7 +155,7 @@ __global__ void __launch_bounds__(BLOCK) k_flat(FlatParams p) {
     const VT* base = vp + t * TILE + threadIdx.x;
     VT v[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) v[u] = ldv(base + u * BLOCK);
+    for (int u = 0; u < U; ++u) v[u] = ldv<HINT>(base + u * BLOCK);
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
@@ -148,7 +164,7 @@ __global__ void __launch_bounds__(BLOCK) k_flat(FlatParams p) {
   // ragged last tile
   for (int64_t i = ntiles * TILE + (int64_t)blockIdx.x * BLOCK + threadIdx.x; i < nv;
        i += (int64_t)gridDim.x * BLOCK) {
-    const VT v = ldv(vp + i);
+    const VT v = ldv<HINT>(vp + i);
 #pragma unroll
     for (int k = 0; k < VW; ++k) acc[k] = R::op(acc[k], R::lift(v.w[k]));
   }
@@ -201,7 +217,7 @@ struct SegParams {
 };
 
 // one warp per row (gang = the grid of warps over rows, vector = the 32 lanes over the row's columns)
-template <class R, int WARPS, int U>
+template <class R, int WARPS, int U, int HINT = 0>
 __global__ void __launch_bounds__(WARPS * 32) k_seg_warp(SegParams p) {
   using B = typename R::B;
   using A = typename R::A;
@@ -225,14 +241,14 @@ __global__ void __launch_bounds__(WARPS * 32) k_seg_warp(SegParams p) {
     for (; i + (U - 1) * 32 < nv; i += U * 32) {
       VT v[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) v[u] = ldv(vp + i + u * 32);
+      for (int u = 0; u < U; ++u) v[u] = ldv<HINT>(vp + i + u * 32);
 #pragma unroll
       for (int u = 0; u < U; ++u)
 #pragma unroll
         for (int k = 0; k < VW; ++k) acc[k] = R::op(acc[k], R::lift(v[u].w[k]));
     }
     for (; i < nv; i += 32) {
-      const VT v = ldv(vp + i);
+      const VT v = ldv<HINT>(vp + i);
 #pragma unroll
       for (int k = 0; k < VW; ++k) acc[k] = R::op(acc[k], R::lift(v.w[k]));
     }
@@ -242,6 +258,134 @@ __global__ void __launch_bounds__(WARPS * 32) k_seg_warp(SegParams p) {
     for (int s = VW / 2; s > 0; s >>= 1)
 #pragma unroll
       for (int k = 0; k < s; ++k) acc[k] = R::op(acc[k], acc[k + s]);
+    A t = R::warp(acc[0]);
+    if (lane == 0) {
+      if (p.has_init) t = R::op(R::lift((B)p.init), t);
+      ((B*)p.out)[r] = R::fin(t);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------ TMA rows
+// One warp per row like k_seg_warp, but the row body is staged into shared memory by the bulk-copy engine
+// (cp.async.bulk ... mbarrier::complete_tx, SASS UBLKCP) through a per-warp ring of S slots of CH bytes; lane
+// 0 keeps S chunks in flight across row boundaries, all 32 lanes fold each landed chunk from shared memory
+// with conflict-free 16-byte loads. Requirements: row bodies split at 16-byte boundaries (head/tail elements
+// of each row are read directly). No CTA-wide barrier: each warp owns its ring and its mbarriers.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t phase) {
+  asm volatile(
+      "{\n.reg .pred P;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      "@!P bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(b)), "l"(0x12F0000000000000ull)  // evict-first policy
+      : "memory");
+}
+
+template <class R, int WARPS, int S, int CH>
+struct SegTma {
+  static constexpr int SMEM = WARPS * S * CH + WARPS * S * 8;
+};
+
+template <class R, int WARPS, int S, int CH>
+__global__ void __launch_bounds__(WARPS * 32) k_seg_tma(SegParams p) {
+  using B = typename R::B;
+  using A = typename R::A;
+  constexpr int EPV = 16 / sizeof(B);  // elements per 16-byte shared-memory load
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned char* ring = smem + (size_t)wid * S * CH;
+  uint64_t* bar = (uint64_t*)(smem + (size_t)WARPS * S * CH) + wid * S;
+  if (lane == 0)
+    for (int i = 0; i < S; ++i) mbar_init(bar + i, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+
+  const int64_t gw = (int64_t)blockIdx.x * WARPS + wid;
+  const int64_t nw = (int64_t)gridDim.x * WARPS;
+  const int es = (int)sizeof(B);
+  // per-row body geometry: [head elements][body: multiple of 16 bytes][tail elements]
+  auto geom = [&](int64_t r, const B*& a, int64_t& head, int64_t& body_bytes) {
+    a = (const B*)p.a + r * p.row_stride;
+    head = (int64_t)(((16u - ((uintptr_t)a & 15u)) & 15u) / es);
+    if (head > p.cols) head = p.cols;
+    body_bytes = ((p.cols - head) * es) & ~(int64_t)15;
+  };
+  // producer cursor (meaningful in lane 0): row, byte offset in the row body
+  int64_t pr = gw, poff = 0;
+  const B* pa;
+  int64_t phead, pbody;
+  if (pr < p.rows) geom(pr, pa, phead, pbody);
+  auto produce = [&](int slot) {  // issue the next chunk into `slot`; returns via cursors
+    while (pr < p.rows && poff >= pbody) {
+      pr += nw;
+      poff = 0;
+      if (pr < p.rows) geom(pr, pa, phead, pbody);
+    }
+    if (pr >= p.rows) return;
+    const uint32_t bytes = (uint32_t)((pbody - poff) < CH ? (pbody - poff) : CH);
+    if (lane == 0) {
+      mbar_expect_tx(bar + slot, bytes);
+      bulk_g2s(ring + (size_t)slot * CH, (const char*)(pa + phead) + poff, bytes, bar + slot);
+    }
+    poff += bytes;
+  };
+  for (int i = 0; i < S; ++i) produce(i);
+
+  int slot = 0;
+  uint32_t phase = 0;
+  for (int64_t r = gw; r < p.rows; r += nw) {
+    const B* a;
+    int64_t head, body;
+    geom(r, a, head, body);
+    A acc[EPV];
+#pragma unroll
+    for (int k = 0; k < EPV; ++k) acc[k] = R::id();
+    for (int64_t off = 0; off < body; off += CH) {
+      const int bytes = (int)((body - off) < CH ? (body - off) : CH);
+      mbar_wait(bar + slot, phase);
+      const unsigned char* c = ring + (size_t)slot * CH;
+      for (int o = lane * 16; o < bytes; o += 32 * 16) {
+        const uint4 q = *(const uint4*)(c + o);
+        if (EPV == 4) {
+          acc[0] = R::op(acc[0], R::lift((B)q.x));
+          acc[1 % EPV] = R::op(acc[1 % EPV], R::lift((B)q.y));
+          acc[2 % EPV] = R::op(acc[2 % EPV], R::lift((B)q.z));
+          acc[3 % EPV] = R::op(acc[3 % EPV], R::lift((B)q.w));
+        } else {
+          acc[0] = R::op(acc[0], R::lift((B)(((uint64_t)q.y << 32) | q.x)));
+          acc[1 % EPV] = R::op(acc[1 % EPV], R::lift((B)(((uint64_t)q.w << 32) | q.z)));
+        }
+      }
+      __syncwarp();
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before the next async write
+      produce(slot);
+      if (++slot == S) {
+        slot = 0;
+        phase ^= 1u;
+      }
+    }
+    // head and tail elements of this row
+    const int64_t tail0 = head + body / es;
+    if (lane < head) acc[0] = R::op(acc[0], R::lift(lds(a + lane)));
+    for (int64_t j = tail0 + lane; j < p.cols; j += 32) acc[EPV - 1] = R::op(acc[EPV - 1], R::lift(lds(a + j)));
+#pragma unroll
+    for (int s2 = EPV / 2; s2 > 0; s2 >>= 1)
+#pragma unroll
+      for (int k = 0; k < s2; ++k) acc[k] = R::op(acc[k], acc[k + s2]);
     A t = R::warp(acc[0]);
     if (lane == 0) {
       if (p.has_init) t = R::op(R::lift((B)p.init), t);

@@ -60,6 +60,7 @@ def _load():
         "ipm_reduce_segmented": ([ci, ci, vp, i64, i64, i64, vp, vp, vp, vp], ci),
         "ipm_reduce_host": ([ci, ci, vp, i64, vp, vp, vp], ci),
         "ipm_release_staging": ([], ci),
+        "ipm_set_option": ([ci, i64], ci),
         "ipm_profile_enable": ([ci], ci),
         "ipm_profile_read": ([vp, vp, ci, ctypes.POINTER(ci)], ci),
         "ipm_profile_disable": ([], ci),
@@ -83,7 +84,7 @@ lib = _load()
 EXPORTED = ("ipm_status_str ipm_last_error_message ipm_op_legal ipm_dtype_size ipm_version ipm_set_allocator "
             "ipm_copyin ipm_create ipm_present ipm_update_device ipm_update_host ipm_copyout ipm_delete "
             "ipm_present_count ipm_workspace_bytes ipm_workspace_init ipm_reduce ipm_reduce_async "
-            "ipm_reduce_segmented ipm_reduce_host ipm_release_staging ipm_profile_enable ipm_profile_read "
+            "ipm_reduce_segmented ipm_reduce_host ipm_release_staging ipm_set_option ipm_profile_enable ipm_profile_read "
             "ipm_profile_disable ipm_flat_geometry ipm_comm_id_bytes "
             "ipm_comm_unique_id ipm_comm_init ipm_comm_destroy ipm_shard_range ipm_reduce_dist "
             "ipm_reduce_dist_async").split()
@@ -256,6 +257,18 @@ def identity_value(op: str, dt: int):
     """The identity of op on element type dt, as the library's own finalize kernel produces it (n = 0)."""
     out = reduce_async(op, torch.empty(0, dtype=TORCH_OF[dt], device="cuda"))
     return out.cpu().numpy()[0]
+
+
+OPTIONS = {"flat_ctas_per_sm": 0, "seg_kernel": 1}
+SEG_KERNELS = {"auto": 0, "ldg": 1, "tma": 2}
+
+
+def set_option(key: str, value) -> None:
+    """Process-wide tuning option (ipm_set_option): flat_ctas_per_sm (1..8, -1 default), seg_kernel
+    ('auto' | 'ldg' | 'tma')."""
+    if key == "seg_kernel" and isinstance(value, str):
+        value = SEG_KERNELS[value]
+    _check(lib.ipm_set_option(OPTIONS[key], int(value)), "ipm_set_option")
 
 
 def flat_geometry(dtype, n: int):

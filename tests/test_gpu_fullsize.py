@@ -1,0 +1,115 @@
+"""GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py times (the library picks the
+same grid for the same n). C1-C4 are compared with the oracle on every element (the oracle takes seconds per
+op); C5 (2^34 float32, 64 GiB) is checked through properties that hold at any size plus the oracle on a
+prefix and on sampled shards."""
+import numpy as np
+import pytest
+import torch
+
+import ipmgen
+import oracle
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+TD = {"int32": torch.int32, "int64": torch.int64, "float32": torch.float32, "float64": torch.float64}
+NPT = {"int32": np.int32, "int64": np.int64, "float32": np.float32, "float64": np.float64}
+TOL = {"float32": 1e-5, "float64": 1e-12}
+
+
+@pytest.fixture(scope="module")
+def ipm():
+    from paper_1412_1127_b200 import ipm as m
+    return m
+
+
+def gen(spec):
+    x = torch.empty(spec.n, dtype=TD[spec.dtype], device="cuda")
+    ipmgen.fill_tensor(spec, x)
+    return x
+
+
+def test_c1(ipm):
+    n = 1 << 20
+    x = gen(ipmgen.Spec("int32", n, "iota", param=1))
+    assert ipm.reduce("+", x, init=np.int32(0)) == 524288          # 2^19 (2^20 + 1) mod 2^32
+    for seed in range(30):
+        spec = ipmgen.Spec("int32", n, "random", seed=seed)
+        x = gen(spec)
+        assert ipm.reduce("+", x) == oracle.reduce("+", x.cpu().numpy())[0]
+
+
+@pytest.mark.parametrize("dt", ["float32", "float64"])
+@pytest.mark.parametrize("op", ["+", "*", "max", "min"])
+def test_c2(ipm, op, dt):
+    n = 1 << 28
+    kind = {"+": "random", "*": "signs", "max": "signed", "min": "signed"}[op]
+    spec = ipmgen.Spec(dt, n, kind, seed=1, plant="factor" if op == "*" else "none", nplant=64 if op == "*" else 0)
+    x = gen(spec)
+    got = ipm.reduce(op, x)
+    want_t, want_ld = oracle.reduce(op, x.cpu().numpy())
+    if op in ("+", "*"):
+        assert abs(np.longdouble(got) - want_ld) <= TOL[dt] * abs(want_ld)
+    else:
+        assert got == want_t
+    if op == "+":  # dyadic grid: every partial sum is exact in fp64 -> the correctly rounded sum
+        assert got == NPT[dt](want_ld)
+
+
+def test_c3(ipm):
+    rows, cols = 65536, 4096
+    spec = ipmgen.Spec("float32", rows * cols, "random", seed=1)
+    x = gen(spec)
+    out = ipm.reduce_segmented("+", x.view(rows, cols)).cpu().numpy()
+    _, want = oracle.reduce_segmented("+", x.cpu().numpy(), rows, cols)
+    # each row is exact in fp64 (4096 dyadic values < 2^24 units of 2^-14): correctly rounded per row
+    assert np.array_equal(out, want.astype(np.float32))
+
+
+@pytest.mark.parametrize("dt", ["int32", "int64"])
+def test_c4(ipm, dt):
+    n = 1 << 30
+    for op in ("&", "|", "^", "&&", "||"):
+        spec = {"&": ipmgen.Spec(dt, n, "allbits", seed=1, plant="clearbit", nplant=8),
+                "|": ipmgen.Spec(dt, n, "const", param=0, seed=1, plant="setbit", nplant=8),
+                "^": ipmgen.Spec(dt, n, "random", seed=1),
+                "&&": ipmgen.Spec(dt, n, "nonzero", seed=1, plant="value", nplant=1, plant_param=0),
+                "||": ipmgen.Spec(dt, n, "const", param=0, seed=1, plant="value", nplant=1, plant_param=3)}[op]
+        x = gen(spec)
+        got = ipm.reduce(op, x)
+        want = oracle.reduce(op, x.cpu().numpy())[0]
+        assert got == want, (op, dt, got, want)
+        del x
+        torch.cuda.empty_cache()
+
+
+def test_c4_odd_residue_product(ipm):
+    # Gauss's generalised Wilson theorem: the product of all 2^31 odd residues mod 2^32 is 1
+    x = torch.arange(1, 1 << 32, 2, dtype=torch.int64, device="cuda").to(torch.int32)  # wraps to int32 words
+    assert ipm.reduce("*", x) == 1
+
+
+def test_c5_properties_and_prefix(ipm):
+    n = 1 << 34
+    x = torch.empty(n, dtype=torch.float32, device="cuda")
+    # exactly-once at full size: Σ 1 = 2^34 (a power of two, exact in fp32)
+    x.fill_(1.0)
+    assert ipm.reduce("+", x) == np.float32(2.0 ** 34)
+    # closed form: a_i = i mod 1024 -> 2^24 * 523776 = 1023 * 2^33, exact in fp32; fp64 partials exact
+    ipmgen.fill_tensor(ipmgen.Spec("float32", n, "mod", param=1024), x)
+    assert ipm.reduce("+", x) == np.float32(1023 * 2.0 ** 33)
+    # the bench workload: the oracle on a 2^28 prefix and on a shard window, same kernel
+    spec = ipmgen.Spec("float32", n, "random", seed=1)
+    ipmgen.fill_tensor(spec, x)
+    for lo, cnt in [(0, 1 << 28), (n - (1 << 27) - 5, (1 << 27) + 5)]:
+        got = ipm.reduce("+", x[lo:lo + cnt])
+        _, want = oracle.reduce("+", x[lo:lo + cnt].cpu().numpy())
+        assert got == np.float32(want)
+    # the whole 2^34: the sum of the per-(2^30) chunk reductions computed by the library in fp64 must agree
+    full = ipm.reduce("+", x)
+    chunks = [ipm.reduce_async("+", x[i:i + (1 << 30)]).double() for i in range(0, n, 1 << 30)]
+    total = float(torch.cat(chunks).sum())
+    assert abs(float(full) - total) <= 1e-6 * total
+    # and the multi-GPU code path at world 1 gives the same bits as the single-GPU call
+    import torch.distributed as dist
+    comm = ipm.Comm(0, 1, torch.cuda.current_device(), store=dist.HashStore())
+    assert comm.reduce("+", x) == full
+    comm.close()

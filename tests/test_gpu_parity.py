@@ -211,8 +211,15 @@ SEG_SHAPES = [(0, 5), (1, 0), (7, 0), (1, 1), (7, 3), (1000, 1), (1000, 3), (100
               (257, 4095), (257, 4096), (65, 4097), (3, 1 << 20), (1, (1 << 21) + 5), (40, 70_001)]
 
 
+@pytest.fixture(params=["ldg", "tma"])
+def seg_kernel(request, ipm):
+    ipm.set_option("seg_kernel", request.param)
+    yield request.param
+    ipm.set_option("seg_kernel", "auto")
+
+
 @pytest.mark.parametrize("op,dt", LEGAL)
-def test_segmented_parity(ipm, op, dt):
+def test_segmented_parity(ipm, op, dt, seg_kernel):
     for k, (rows, cols) in enumerate(SEG_SHAPES):
         stride = cols + (k % 3) * 5  # row_stride >= cols, also non-multiples of the vector width
         total = max(0, (rows - 1) * stride + cols) if rows else 0
@@ -228,7 +235,7 @@ def test_segmented_parity(ipm, op, dt):
             assert out.tobytes() == want_t.tobytes(), (op, dt, rows, cols)
 
 
-def test_segmented_row_constant_closed_form(ipm):
+def test_segmented_row_constant_closed_form(ipm, seg_kernel):
     rows, cols = 4096, 4096
     spec = ipmgen.Spec("float32", rows * cols, "const", param=0)
     x = device_input(spec)

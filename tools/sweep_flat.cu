@@ -1,0 +1,149 @@
+// sweep_flat.cu — tuning experiment (not product): times the product's k_flat / k_seg_warp templates over
+// block size, loads in flight (U), cache hint and CTAs per SM, on large inputs, with CUDA events.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include -I paper_1412_1127_b200/csrc
+//        -o build/sweep_flat tools/sweep_flat.cu
+#include <cuda_runtime.h>
+#include <algorithm>
+#include <cstdio>
+#include <functional>
+#include <string>
+#include <vector>
+#include "ipm_kernels.cuh"
+
+using namespace ipm;
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s at %d\n", cudaGetErrorString(e), __LINE__); exit(1);} } while (0)
+
+static float time_ms(std::function<void()> f, int reps) {
+  for (int i = 0; i < 3; ++i) f();
+  CK(cudaDeviceSynchronize());
+  std::vector<float> v;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a); cudaEventCreate(&b);
+  for (int i = 0; i < reps; ++i) {
+    cudaEventRecord(a); f(); cudaEventRecord(b); cudaEventSynchronize(b);
+    float ms; cudaEventElapsedTime(&ms, a, b); v.push_back(ms);
+  }
+  std::sort(v.begin(), v.end());
+  return v[v.size() / 2];
+}
+
+template <class R, int BLOCK, int U, int HINT>
+void run_flat(const char* name, void* buf, size_t bytes, void* ws, int sms) {
+  int maxb = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&maxb, k_flat<R, BLOCK, U, HINT>, BLOCK, 0));
+  const int64_t n = bytes / sizeof(typename R::B);
+  for (int cps = 1; cps <= maxb; cps *= 2) {
+    FlatParams p{};
+    p.a = buf; p.n = n; p.row_stride = 0; p.init = 0; p.has_init = 0; p.mode = MODE_PARTIAL;
+    p.out = (char*)ws + 4160; p.partials = (uint64_t*)((char*)ws + 8192); p.tickets = (unsigned*)ws;
+    const int grid = sms * cps;
+    float ms = time_ms([&] { k_flat<R, BLOCK, U, HINT><<<grid, BLOCK>>>(p); }, 10);
+    CK(cudaGetLastError());
+    printf("flat %-10s B=%4d U=%d H=%d cps=%d grid=%5d  %7.3f ms  %7.1f GB/s\n", name, BLOCK, U, HINT, cps, grid, ms,
+           bytes / ms / 1e6);
+  }
+}
+
+template <class R, int WARPS, int U, int HINT>
+void run_seg(const char* name, void* buf, void* out, int sms) {
+  int maxb = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&maxb, k_seg_warp<R, WARPS, U, HINT>, WARPS * 32, 0));
+  const int64_t rows = 65536, cols = 4096;
+  for (int cps = 1; cps <= maxb; cps *= 2) {
+    SegParams p{buf, rows, cols, cols, 0, 0, out};
+    const int grid = std::min<int64_t>(sms * cps, (rows + WARPS - 1) / WARPS);
+    float ms = time_ms([&] { k_seg_warp<R, WARPS, U, HINT><<<grid, WARPS * 32>>>(p); }, 10);
+    CK(cudaGetLastError());
+    printf("seg  %-10s W=%2d U=%d H=%d cps=%d grid=%5d  %7.3f ms  %7.1f GB/s\n", name, WARPS, U, HINT, cps, grid, ms,
+           (rows * cols * 4.0 + rows * 4) / ms / 1e6);
+  }
+}
+
+template <class R, int WARPS, int S, int CH>
+void run_seg_tma(const char* name, void* buf, void* out, int sms, int64_t rows, int64_t cols) {
+  constexpr int smem = SegTma<R, WARPS, S, CH>::SMEM;
+  CK(cudaFuncSetAttribute(k_seg_tma<R, WARPS, S, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  int maxb = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&maxb, k_seg_tma<R, WARPS, S, CH>, WARPS * 32, smem));
+  for (int cps = 1; cps <= maxb; cps *= 2) {
+    SegParams p{buf, rows, cols, cols, 0, 0, out};
+    const int grid = std::min<int64_t>(sms * cps, (rows + WARPS - 1) / WARPS);
+    float ms = time_ms([&] { k_seg_tma<R, WARPS, S, CH><<<grid, WARPS * 32, smem>>>(p); }, 10);
+    CK(cudaGetLastError());
+    printf("tma  %-10s W=%2d S=%d CH=%5d cps=%d grid=%5d rows=%ld cols=%ld %7.3f ms  %7.1f GB/s\n", name, WARPS, S, CH, cps,
+           grid, (long)rows, (long)cols, ms, (rows * cols * 4.0 + rows * 4) / ms / 1e6);
+  }
+}
+
+int main(int argc, char** argv) {
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  const size_t big = (size_t)16 << 30;
+  void* buf; void* ws; void* out;
+  CK(cudaMalloc(&buf, big));
+  CK(cudaMemset(buf, 1, big));
+  CK(cudaMalloc(&ws, 1 << 20));
+  CK(cudaMemset(ws, 0, 1 << 20));
+  CK(cudaMalloc(&out, 1 << 20));
+  const std::string mode = argc > 1 ? argv[1] : "all";
+  for (size_t bytes : {(size_t)1 << 30, (size_t)4 << 30, (size_t)16 << 30}) {
+    printf("== %zu GiB\n", bytes >> 30);
+    if (mode == "all" || mode == "hint") {
+      run_flat<Red<IPM_ADD, IPM_F32>, 256, 4, 0>("f32+", buf, bytes, ws, sms);
+      run_flat<Red<IPM_ADD, IPM_F32>, 256, 4, 1>("f32+", buf, bytes, ws, sms);
+      run_flat<Red<IPM_ADD, IPM_F32>, 256, 4, 2>("f32+", buf, bytes, ws, sms);
+      run_flat<Red<IPM_ADD, IPM_F32>, 256, 4, 3>("f32+", buf, bytes, ws, sms);
+      run_flat<Red<IPM_BXOR, IPM_I32>, 256, 4, 0>("i32^", buf, bytes, ws, sms);
+      run_flat<Red<IPM_BXOR, IPM_I32>, 256, 4, 1>("i32^", buf, bytes, ws, sms);
+      run_flat<Red<IPM_BXOR, IPM_I64>, 256, 4, 0>("i64^", buf, bytes, ws, sms);
+      run_flat<Red<IPM_BXOR, IPM_I64>, 256, 4, 1>("i64^", buf, bytes, ws, sms);
+    }
+    if (mode == "all" || mode == "shape") {
+      run_flat<Red<IPM_ADD, IPM_F32>, 256, 2, 0>("f32+", buf, bytes, ws, sms);
+      run_flat<Red<IPM_ADD, IPM_F32>, 256, 8, 0>("f32+", buf, bytes, ws, sms);
+      run_flat<Red<IPM_ADD, IPM_F32>, 512, 4, 0>("f32+", buf, bytes, ws, sms);
+      run_flat<Red<IPM_ADD, IPM_F32>, 1024, 2, 0>("f32+", buf, bytes, ws, sms);
+      run_flat<Red<IPM_ADD, IPM_F32>, 128, 8, 0>("f32+", buf, bytes, ws, sms);
+      run_flat<Red<IPM_BXOR, IPM_I32>, 256, 8, 0>("i32^", buf, bytes, ws, sms);
+      run_flat<Red<IPM_BXOR, IPM_I32>, 512, 4, 0>("i32^", buf, bytes, ws, sms);
+      run_flat<Red<IPM_BXOR, IPM_I32>, 1024, 4, 0>("i32^", buf, bytes, ws, sms);
+      run_flat<Red<IPM_ADD, IPM_F64>, 256, 4, 0>("f64+", buf, bytes, ws, sms);
+      run_flat<Red<IPM_ADD, IPM_F64>, 256, 8, 0>("f64+", buf, bytes, ws, sms);
+      run_flat<Red<IPM_MAX, IPM_F64>, 256, 4, 0>("f64max", buf, bytes, ws, sms);
+    }
+  }
+  if (mode == "all" || mode == "seg") {
+    printf("== segmented 65536 x 4096 f32\n");
+    run_seg<Red<IPM_ADD, IPM_F32>, 8, 4, 0>("f32+", buf, out, sms);
+    run_seg<Red<IPM_ADD, IPM_F32>, 8, 2, 0>("f32+", buf, out, sms);
+    run_seg<Red<IPM_ADD, IPM_F32>, 8, 8, 0>("f32+", buf, out, sms);
+    run_seg<Red<IPM_ADD, IPM_F32>, 4, 4, 0>("f32+", buf, out, sms);
+    run_seg<Red<IPM_ADD, IPM_F32>, 16, 4, 0>("f32+", buf, out, sms);
+    run_seg<Red<IPM_ADD, IPM_F32>, 8, 4, 1>("f32+", buf, out, sms);
+  }
+  if (mode == "all" || mode == "seg" || mode == "tma") {
+    printf("== TMA segmented\n");
+    for (int64_t cols : {4096, 65536}) {
+      const int64_t rows = (int64_t)65536 * 4096 / cols;
+      run_seg_tma<Red<IPM_ADD, IPM_F32>, 8, 4, 4096>("f32+", buf, out, sms, rows, cols);
+      run_seg_tma<Red<IPM_ADD, IPM_F32>, 8, 2, 8192>("f32+", buf, out, sms, rows, cols);
+      run_seg_tma<Red<IPM_ADD, IPM_F32>, 4, 4, 8192>("f32+", buf, out, sms, rows, cols);
+      run_seg_tma<Red<IPM_ADD, IPM_F32>, 8, 8, 2048>("f32+", buf, out, sms, rows, cols);
+      run_seg_tma<Red<IPM_ADD, IPM_F32>, 4, 8, 4096>("f32+", buf, out, sms, rows, cols);
+      run_seg_tma<Red<IPM_ADD, IPM_F32>, 2, 8, 8192>("f32+", buf, out, sms, rows, cols);
+    }
+  }
+  if (mode == "all" || mode == "big") {
+    printf("== flat variants at 16 GiB\n");
+    const size_t bytes = (size_t)16 << 30;
+    run_flat<Red<IPM_ADD, IPM_F32>, 1024, 4, 0>("f32+", buf, bytes, ws, sms);
+    run_flat<Red<IPM_ADD, IPM_F32>, 512, 8, 0>("f32+", buf, bytes, ws, sms);
+    run_flat<Red<IPM_ADD, IPM_F64>, 1024, 4, 0>("f64+", buf, bytes, ws, sms);
+    run_flat<Red<IPM_MAX, IPM_F32>, 1024, 4, 0>("f32max", buf, bytes, ws, sms);
+    run_flat<Red<IPM_MAX, IPM_F32>, 256, 4, 0>("f32max", buf, bytes, ws, sms);
+    run_flat<Red<IPM_MUL, IPM_I64>, 256, 4, 0>("i64*", buf, bytes, ws, sms);
+    run_flat<Red<IPM_MUL, IPM_I64>, 1024, 4, 0>("i64*", buf, bytes, ws, sms);
+  }
+  return 0;
+}
