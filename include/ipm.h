@@ -139,6 +139,48 @@ ipm_status ipm_reduce_segmented(ipm_op op, ipm_dtype dt, const void* dev, int64_
                                 int64_t row_stride, const void* init, void* dev_out, void* workspace,
                                 void* stream);
 
+/* The two levels of the paper's scheme as separate calls ("reducing along threads of thread
+ * block on GPU and reducing along thread block on CPU"; the CUDA SRAD variant it compares against merges on the
+ * GPU with "multiple serial kernel launches"). Used by tools/ablation_twolevel.py to measure that design
+ * point against the one-launch path; ipm_reduce does both levels in one kernel.
+ *   ipm_reduce_partials: one partial per thread block of the flat kernel, written to dev_partials as 8-byte
+ *     slots holding the op's accumulator (for + and * on float32/float64 a double; for integer + * & | ^ and
+ *     the logical ops the unsigned word, zero-extended; for integer max/min the signed word, sign-extended);
+ *     *count = number of blocks (<= max_partials, else IPM_E_SIZE; ipm_flat_geometry gives it in advance).
+ *   ipm_finalize_partials: one-warp kernel: *dev_result = init ⊕ slot[0] ⊕ ... ⊕ slot[count-1] (index order). */
+ipm_status ipm_reduce_partials(ipm_op op, ipm_dtype dt, const void* dev, int64_t n, void* dev_partials,
+                               int max_partials, int* count, void* stream);
+ipm_status ipm_finalize_partials(ipm_op op, ipm_dtype dt, const void* dev_partials, int count, const void* init,
+                                 void* dev_result, void* stream);
+
+/* One scalar over a strided 2-D region: a gang loop over rows collapsed with the
+ * vector loop over columns (SPEC.md:148 nest depth <= 2),
+ *   *inout = *inout ⊕ fold_{r<rows, j<cols} dev[r*row_stride + j]
+ * Rows need not be contiguous (row_stride >= cols) nor aligned beyond the element size. One kernel launch
+ * (the flat kernel when row_stride == cols). rows or cols == 0 -> init ⊕ identity. */
+ipm_status ipm_reduce_2d(ipm_op op, ipm_dtype dt, const void* dev, int64_t rows, int64_t cols, int64_t row_stride,
+                         void* inout, void* workspace, void* stream);
+ipm_status ipm_reduce_2d_async(ipm_op op, ipm_dtype dt, const void* dev, int64_t rows, int64_t cols,
+                               int64_t row_stride, const void* init, void* dev_result, void* workspace,
+                               void* stream);
+
+/* Several reduction variables over ONE pass: a loop that carries more than one
+ * reduction variable (">=1 scalar variable"; SPEC.md:253 a reduction list per kernel) and folds an
+ * expression of the element — SRAD's reduction region accumulates the image's sum and sum of squares
+ * (PAPER.md:205). Signatures (vars in this order; + wraps for integers, float32 expressions and sums in float64):
+ *   IPM_FUSED_SUM_SUMSQ  v0 += x[i];      v1 += x[i]*x[i]
+ *   IPM_FUSED_DOT        v0 += x[i]*y[i]                         (y: a second array, same n)
+ *   IPM_FUSED_MINMAX     v0 = min(v0, x[i]); v1 = max(v1, x[i])   (float: IEEE 754-2019 minimum/maximum)
+ *   IPM_FUSED_STATS      v0 += x; v1 += x*x; v2 = min; v3 = max
+ * x, y: device arrays of n elements of dt; init / inout: host arrays of ipm_fused_nvars(f) elements (init
+ * NULL = identities); dev_result: device array of nvars elements. One kernel launch. */
+typedef enum { IPM_FUSED_SUM_SUMSQ = 0, IPM_FUSED_DOT, IPM_FUSED_MINMAX, IPM_FUSED_STATS } ipm_fused;
+int ipm_fused_nvars(ipm_fused f);
+ipm_status ipm_reduce_fused(ipm_fused f, ipm_dtype dt, const void* x, const void* y, int64_t n, void* inout,
+                            void* workspace, void* stream);
+ipm_status ipm_reduce_fused_async(ipm_fused f, ipm_dtype dt, const void* x, const void* y, int64_t n,
+                                  const void* init, void* dev_result, void* workspace, void* stream);
+
 /* End-to-end clause over a HOST array: the data clause `copyin(a[0:n])` fused with the reduction. The host
  * array is streamed to the device in chunks through two library-owned staging buffers (allocated once
  * through the allocator hook and kept until ipm_release_staging), each chunk's H2D copy overlapping the

@@ -44,6 +44,10 @@ def lib():
         L.ora_reduce.restype = ci
         L.ora_reduce_segmented.argtypes = [ci, ci, vp, i64, i64, i64, vp, vp, vp]
         L.ora_reduce_segmented.restype = ci
+        L.ora_fused_nvars.argtypes = [ci]
+        L.ora_fused_nvars.restype = ci
+        L.ora_reduce_fused.argtypes = [ci, ci, vp, vp, i64, vp, vp, vp]
+        L.ora_reduce_fused.restype = ci
         _lib = L
     return _lib
 
@@ -120,3 +124,28 @@ def reduce_segmented(op: str, a, rows: int, cols: int, stride: int | None = None
 
 def identity(op: str, dtype: str):
     return reduce(op, np.zeros(0, dtype=NP[dtype]), dtype)[0]
+
+
+FUSED = {"sum_sumsq": 0, "dot": 1, "minmax": 2, "stats": 3}
+
+
+def reduce_fused(sig: str, x, y=None, dtype: str | None = None, init=None):
+    """Several variables over one pass: returns (values as a T array, long double array), one per variable.
+    sum_sumsq -> (Σx, Σx²); dot -> (Σxy,); minmax -> (min, max); stats -> (Σx, Σx², min, max)."""
+    x = np.ascontiguousarray(x)
+    dtype = dtype or x.dtype.name
+    x = x.astype(NP[dtype], copy=False)
+    f = FUSED[sig]
+    nv = lib().ora_fused_nvars(f)
+    yy = None if y is None else np.ascontiguousarray(y, dtype=NP[dtype])
+    if f == 1 and (yy is None or yy.size != x.size):
+        raise ValueError("dot needs y of the same length")
+    out = np.zeros(nv, dtype=NP[dtype])
+    out_ld = np.zeros(nv, dtype=np.longdouble)
+    ib = None if init is None else np.ascontiguousarray(init, dtype=NP[dtype])
+    rc = lib().ora_reduce_fused(f, DTYPES[dtype], x.ctypes.data if x.size else None,
+                                None if yy is None or not yy.size else yy.ctypes.data, x.size,
+                                None if ib is None else ib.ctypes.data, out.ctypes.data, out_ld.ctypes.data)
+    if rc:
+        raise ValueError(f"ora_reduce_fused failed ({rc})")
+    return out, out_ld

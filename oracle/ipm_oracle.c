@@ -112,40 +112,48 @@ static double ieee_minimum(double a, double b) {
   return (b < a) ? b : a;
 }
 
-/* one step of the left fold: r = r ⊕ x (x = element i of array p) */
-static void step(ora_state* st, const void* p, int64_t i) {
+/* one step of the left fold on an integer word x (w bits, unsigned representation): r = r ⊕ x */
+static void fold_int(ora_state* st, uint64_t x) {
   const int dt = st->dt;
-  if (!is_float(dt)) {
-    const uint64_t x = int_at(dt, p, i), M = wmask(dt);
-    switch (st->op) {
-      case O_ADD: st->r = (st->r + x) & M; break;                 /* R3: wraps mod 2^w */
-      case O_MUL: st->r = (st->r * x) & M; break;                 /* R3 */
-      case O_MAX: if (as_signed(dt, x) > as_signed(dt, st->r)) st->r = x; break;
-      case O_MIN: if (as_signed(dt, x) < as_signed(dt, st->r)) st->r = x; break;
-      case O_BAND: st->r &= x; break;
-      case O_BOR: st->r |= x; break;
-      case O_BXOR: st->r ^= x; break;
-      case O_LAND: st->r = (st->r != 0) && (x != 0); break;       /* no short circuit: every a[i] is read */
-      case O_LOR: st->r = (st->r != 0) || (x != 0); break;
-    }
-  } else {
-    const double x = flt_at(dt, p, i);
-    switch (st->op) {
-      case O_ADD: { /* Neumaier's improved Kahan–Babuška summation in long double (R7) */
-        const long double xl = (long double)x, t = st->s + xl;
-        if (fabsl(st->s) >= fabsl(xl)) st->c += (st->s - t) + xl;
-        else st->c += (xl - t) + st->s;
-        st->s = t;
-        break;
-      }
-      case O_MUL: st->s *= (long double)x; break;
-      case O_MAX: st->m = ieee_maximum(st->m, x); break;
-      case O_MIN: st->m = ieee_minimum(st->m, x); break;
-      case O_LAND: st->r = (st->r != 0) && (x != 0.0); break;     /* C truthiness: -0.0 false, NaN true */
-      case O_LOR: st->r = (st->r != 0) || (x != 0.0); break;
-    }
+  const uint64_t M = wmask(dt);
+  x &= M;
+  switch (st->op) {
+    case O_ADD: st->r = (st->r + x) & M; break;                 /* R3: wraps mod 2^w */
+    case O_MUL: st->r = (st->r * x) & M; break;                 /* R3 */
+    case O_MAX: if (as_signed(dt, x) > as_signed(dt, st->r)) st->r = x; break;
+    case O_MIN: if (as_signed(dt, x) < as_signed(dt, st->r)) st->r = x; break;
+    case O_BAND: st->r &= x; break;
+    case O_BOR: st->r |= x; break;
+    case O_BXOR: st->r ^= x; break;
+    case O_LAND: st->r = (st->r != 0) && (x != 0); break;       /* no short circuit: every a[i] is read */
+    case O_LOR: st->r = (st->r != 0) || (x != 0); break;
   }
   st->count++;
+}
+
+/* one step of the left fold on a real value x (an element, or an expression of elements, in long double) */
+static void fold_flt(ora_state* st, long double xl) {
+  switch (st->op) {
+    case O_ADD: { /* Neumaier's improved Kahan–Babuška summation in long double (R7) */
+      const long double t = st->s + xl;
+      if (fabsl(st->s) >= fabsl(xl)) st->c += (st->s - t) + xl;
+      else st->c += (xl - t) + st->s;
+      st->s = t;
+      break;
+    }
+    case O_MUL: st->s *= xl; break;
+    case O_MAX: st->m = ieee_maximum(st->m, (double)xl); break;   /* elements only: exact in double */
+    case O_MIN: st->m = ieee_minimum(st->m, (double)xl); break;
+    case O_LAND: st->r = (st->r != 0) && (xl != 0.0L); break;     /* C truthiness: -0.0 false, NaN true */
+    case O_LOR: st->r = (st->r != 0) || (xl != 0.0L); break;
+  }
+  st->count++;
+}
+
+/* one step of the left fold: r = r ⊕ x (x = element i of array p) */
+static void step(ora_state* st, const void* p, int64_t i) {
+  if (!is_float(st->dt)) fold_int(st, int_at(st->dt, p, i));
+  else fold_flt(st, (long double)flt_at(st->dt, p, i));
 }
 
 /* start the fold from the variable's original value (R1); init == NULL means the op's identity */
@@ -217,5 +225,49 @@ int ora_reduce_segmented(int op, int dt, const void* a, int64_t rows, int64_t co
     ora_fold(&st, (const char*)a + (size_t)(r * stride) * es, cols);
     ora_result(&st, out ? (char*)out + (size_t)r * es : 0, out_ld ? out_ld + r : 0);
   }
+  return 0;
+}
+
+/* several reduction variables over one pass (PAPER.md:205 SRAD's
+ * statistics): variable v folds expression e_v(x[i], y[i]) with operator op_v, all in index order.
+ * Expressions (R13): integers — the product wraps mod 2^w; floats — the exact real product,
+ * formed in long double (exact for float32 operands, one rounding at 2^-64 for float64 operands).
+ * Signatures: 0 SUM_SUMSQ {+:x, +:x*x}; 1 DOT {+:x*y}; 2 MINMAX {min:x, max:x}; 3 STATS {+:x, +:x*x, min:x, max:x} */
+enum { E_X = 0, E_XX, E_XY };
+static int sig_vars(int f, int* ops, int* ex) {
+  switch (f) {
+    case 0: ops[0] = O_ADD; ex[0] = E_X; ops[1] = O_ADD; ex[1] = E_XX; return 2;
+    case 1: ops[0] = O_ADD; ex[0] = E_XY; return 1;
+    case 2: ops[0] = O_MIN; ex[0] = E_X; ops[1] = O_MAX; ex[1] = E_X; return 2;
+    case 3: ops[0] = O_ADD; ex[0] = E_X; ops[1] = O_ADD; ex[1] = E_XX; ops[2] = O_MIN; ex[2] = E_X;
+            ops[3] = O_MAX; ex[3] = E_X; return 4;
+  }
+  return 0;
+}
+
+int ora_fused_nvars(int f) { int o[4], e[4]; return sig_vars(f, o, e); }
+
+int ora_reduce_fused(int f, int dt, const void* x, const void* y, int64_t n, const void* init, void* out,
+                     long double* out_ld) {
+  int ops[4], ex[4];
+  const int nv = sig_vars(f, ops, ex);
+  if (!nv || dt < 0 || dt >= T_NTYPES || n < 0) return 1;
+  const int es = (dt == T_I32 || dt == T_F32) ? 4 : 8;
+  ora_state st[4];
+  for (int v = 0; v < nv; ++v) ora_begin(&st[v], ops[v], dt, init ? (const char*)init + v * es : 0);
+  for (int64_t i = 0; i < n; ++i) {
+    for (int v = 0; v < nv; ++v) {
+      if (!is_float(dt)) {
+        const uint64_t a = int_at(dt, x, i), b = ex[v] == E_XY ? int_at(dt, y, i) : a;
+        fold_int(&st[v], ex[v] == E_X ? a : a * b);
+      } else {
+        const long double a = (long double)flt_at(dt, x, i);
+        const long double b = ex[v] == E_XY ? (long double)flt_at(dt, y, i) : a;
+        fold_flt(&st[v], ex[v] == E_X ? a : a * b);
+      }
+    }
+  }
+  for (int v = 0; v < nv; ++v)
+    ora_result(&st[v], out ? (char*)out + v * es : 0, out_ld ? out_ld + v : 0);
   return 0;
 }

@@ -13,6 +13,7 @@
 #include "ipm.h"
 #include "ipm_internal.h"
 #include "ipm_kernels.cuh"
+#include "ipm_fused.cuh"
 
 namespace ipm {
 
@@ -156,6 +157,9 @@ struct Launch {
   static void seg_warp(const SegParams& p, int grid, cudaStream_t st) {
     k_seg_warp<R, SEG_WARPS, SEG_U><<<grid, SEG_WARPS * 32, 0, st>>>(p);
   }
+  static void two_d(const Params2D& q, int grid, cudaStream_t st) {
+    k_2d<R, FLAT_BLOCK, 4><<<grid, FLAT_BLOCK, 0, st>>>(q);
+  }
   static cudaError_t seg_tma(const SegParams& p, int grid, cudaStream_t st) {
     constexpr int smem = SegTma<R, TMA_WARPS, TMA_S, TMA_CH>::SMEM;
     static cudaError_t attr =
@@ -180,6 +184,7 @@ struct Launch {
 
 struct Table {
   void (*flat)(const FlatParams&, dim3, cudaStream_t);
+  void (*two_d)(const Params2D&, int, cudaStream_t);
   void (*seg_warp)(const SegParams&, int, cudaStream_t);
   cudaError_t (*seg_tma)(const SegParams&, int, cudaStream_t);
   void (*seg_group)(const SegParams&, int, int, cudaStream_t);
@@ -189,7 +194,7 @@ struct Table {
 static const Table* table(ipm_op op, ipm_dtype dt) {
 #define IPM_ENTRY(O, D)                                                                                  \
   if (op == O && dt == D) {                                                                            \
-    static const Table t = {&Launch<O, D>::flat, &Launch<O, D>::seg_warp, &Launch<O, D>::seg_tma,     \
+    static const Table t = {&Launch<O, D>::flat, &Launch<O, D>::two_d, &Launch<O, D>::seg_warp, &Launch<O, D>::seg_tma,     \
                             &Launch<O, D>::seg_group, &Launch<O, D>::finalize};                        \
     return &t;                                                                                         \
   }
@@ -248,6 +253,40 @@ ipm_status launch_finalize(ipm_op op, ipm_dtype dt, const uint64_t* slots, int P
   table(op, dt)->finalize(slots, P, init, has_init, out, st);
   CK(cudaGetLastError());
   return IPM_OK;
+}
+
+// ------------------------------------------------------------------------------------------ fused
+template <int DT>
+struct FusedLaunch {
+  using ADDX = Comp<Red<IPM_ADD, DT>, EX>;
+  using ADDXX = Comp<Red<IPM_ADD, DT>, EXX>;
+  using ADDXY = Comp<Red<IPM_ADD, DT>, EXY>;
+  using MINX = Comp<Red<IPM_MIN, DT>, EX>;
+  using MAXX = Comp<Red<IPM_MAX, DT>, EX>;
+  template <class C0, class C1, class C2, class C3, bool TWO>
+  static void go(const FusedParams& p, bool vec, int grid, cudaStream_t st) {
+    using S = Sig<C0, C1, C2, C3>;
+    if (vec) k_fused<S, C0, C1, C2, C3, TWO, true, FLAT_BLOCK, 2><<<grid, FLAT_BLOCK, 0, st>>>(p);
+    else k_fused<S, C0, C1, C2, C3, TWO, false, FLAT_BLOCK, 2><<<grid, FLAT_BLOCK, 0, st>>>(p);
+  }
+  static void launch(ipm_fused f, const FusedParams& p, bool vec, int grid, cudaStream_t st) {
+    switch (f) {
+      case IPM_FUSED_SUM_SUMSQ: go<ADDX, ADDXX, NoComp, NoComp, false>(p, vec, grid, st); break;
+      case IPM_FUSED_DOT: go<ADDXY, NoComp, NoComp, NoComp, true>(p, vec, grid, st); break;
+      case IPM_FUSED_MINMAX: go<MINX, MAXX, NoComp, NoComp, false>(p, vec, grid, st); break;
+      case IPM_FUSED_STATS: go<ADDX, ADDXX, MINX, MAXX, false>(p, vec, grid, st); break;
+    }
+  }
+};
+
+static int fused_nvars(ipm_fused f) {
+  switch (f) {
+    case IPM_FUSED_SUM_SUMSQ: return 2;
+    case IPM_FUSED_DOT: return 1;
+    case IPM_FUSED_MINMAX: return 2;
+    case IPM_FUSED_STATS: return 4;
+  }
+  return 0;
 }
 
 // ------------------------------------------------------------------------------------------ allocator
@@ -532,6 +571,189 @@ ipm_status ipm_reduce_segmented(ipm_op op, ipm_dtype dt, const void* dev, int64_
     t->seg_group(p, G, (int)std::max<int64_t>(1, blocks), st);
   }
   CK(cudaGetLastError());
+  return IPM_OK;
+}
+
+// ---------------------------------------------------------------------------------- two-level pieces
+ipm_status ipm_reduce_partials(ipm_op op, ipm_dtype dt, const void* dev, int64_t n, void* dev_partials,
+                               int max_partials, int* count, void* stream) {
+  ipm_status s;
+  if ((s = validate(op, dt)) || (s = check_array(dt, dev, n))) return s;
+  if (!dev_partials || !count) {
+    set_error("NULL pointer");
+    return IPM_E_NULL;
+  }
+  const int g = (int)flat_grid(dt, n);
+  if (max_partials < g) {
+    set_error("max_partials smaller than the grid (query ipm_flat_geometry)");
+    return IPM_E_SIZE;
+  }
+  FlatParams p;
+  p.a = dev;
+  p.n = n;
+  p.row_stride = 0;
+  p.init = 0;
+  p.has_init = 0;
+  p.mode = MODE_CTA_PARTIALS;
+  p.out = dev_partials;
+  p.partials = nullptr;
+  p.tickets = nullptr;
+  cudaStream_t st = (cudaStream_t)stream;
+  {
+    ProfScope ps(st, 0);
+    table(op, dt)->flat(p, dim3((unsigned)g, 1, 1), st);
+  }
+  CK(cudaGetLastError());
+  *count = g;
+  return IPM_OK;
+}
+
+ipm_status ipm_finalize_partials(ipm_op op, ipm_dtype dt, const void* dev_partials, int count, const void* init,
+                                 void* dev_result, void* stream) {
+  ipm_status s;
+  if ((s = validate(op, dt))) return s;
+  if ((count > 0 && !dev_partials) || !dev_result) {
+    set_error("NULL pointer");
+    return IPM_E_NULL;
+  }
+  if (count < 0) {
+    set_error("negative count");
+    return IPM_E_SIZE;
+  }
+  return launch_finalize(op, dt, (const uint64_t*)dev_partials, count, scalar_bits(dt, init), init != nullptr,
+                         dev_result, (cudaStream_t)stream);
+}
+
+// ---------------------------------------------------------------------------------- 2-D collapse
+ipm_status ipm_reduce_2d_async(ipm_op op, ipm_dtype dt, const void* dev, int64_t rows, int64_t cols,
+                               int64_t row_stride, const void* init, void* dev_result, void* ws, void* stream) {
+  ipm_status s;
+  if ((s = validate(op, dt)) || (s = check_ws(ws))) return s;
+  if (rows < 0 || cols < 0 || row_stride < cols) {
+    set_error("need rows >= 0, cols >= 0, row_stride >= cols");
+    return IPM_E_SIZE;
+  }
+  if (row_stride > 0 && rows > 0 && (rows - 1) > (INT64_MAX - cols) / row_stride) {
+    set_error("rows*row_stride overflows");
+    return IPM_E_SIZE;
+  }
+  if (rows * cols > 0 && !dev) {
+    set_error("NULL device array");
+    return IPM_E_NULL;
+  }
+  if (!dev_result) {
+    set_error("NULL dev_result");
+    return IPM_E_NULL;
+  }
+  if (dev && ((uintptr_t)dev % esize(dt))) {
+    set_error("device array not aligned to its element size");
+    return IPM_E_ALIGN;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint64_t ib = scalar_bits(dt, init);
+  if (rows == 0 || cols == 0) return launch_finalize(op, dt, nullptr, 0, ib, init != nullptr, dev_result, st);
+  if (row_stride == cols || rows == 1)  // contiguous region: the flat clause
+    return launch_flat(op, dt, dev, rows * cols, ib, init != nullptr, MODE_RESULT, dev_result, ws, st);
+  Params2D q;
+  q.f.a = dev;
+  q.f.n = 0;
+  q.f.row_stride = 0;
+  q.f.init = ib;
+  q.f.has_init = init != nullptr;
+  q.f.mode = MODE_RESULT;
+  q.f.out = dev_result;
+  q.f.partials = (uint64_t*)((char*)ws + WS_PARTIALS);
+  q.f.tickets = (unsigned*)((char*)ws + WS_TICKETS);
+  q.rows = rows;
+  q.cols = cols;
+  q.row_stride = row_stride;
+  const int64_t vw = 32 / (int64_t)esize(dt), chv = 32 * 4;
+  const int64_t per_row = std::max<int64_t>(1, (cols / vw + chv - 1) / chv);
+  const int64_t items = rows * per_row;
+  const int64_t grid = std::max<int64_t>(
+      1, std::min<int64_t>((int64_t)sm_count() * flat_ctas_per_sm(), (items + FLAT_BLOCK / 32 - 1) / (FLAT_BLOCK / 32)));
+  {
+    ProfScope ps(st, 3);
+    table(op, dt)->two_d(q, (int)grid, st);
+  }
+  CK(cudaGetLastError());
+  return IPM_OK;
+}
+
+ipm_status ipm_reduce_2d(ipm_op op, ipm_dtype dt, const void* dev, int64_t rows, int64_t cols, int64_t row_stride,
+                         void* inout, void* ws, void* stream) {
+  if (!inout) {
+    set_error("NULL inout");
+    return IPM_E_NULL;
+  }
+  void* res = (char*)ws + WS_RESULT;
+  ipm_status s = ipm_reduce_2d_async(op, dt, dev, rows, cols, row_stride, inout, res, ws, stream);
+  if (s) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaMemcpyAsync(inout, res, esize(dt), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return IPM_OK;
+}
+
+// ---------------------------------------------------------------------------------- fused (multi-variable)
+int ipm_fused_nvars(ipm_fused f) { return fused_nvars(f); }
+
+ipm_status ipm_reduce_fused_async(ipm_fused f, ipm_dtype dt, const void* x, const void* y, int64_t n,
+                                  const void* init, void* dev_result, void* ws, void* stream) {
+  ipm_status s;
+  const int nv = fused_nvars(f);
+  if (!nv) {
+    set_error("unknown fused signature");
+    return IPM_E_ARG;
+  }
+  if (!esize(dt)) {
+    set_error("unknown dtype");
+    return IPM_E_DTYPE;
+  }
+  if ((s = check_array(dt, x, n)) || (s = check_ws(ws))) return s;
+  if (f == IPM_FUSED_DOT && (s = check_array(dt, y, n))) return s;
+  if (!dev_result) {
+    set_error("NULL dev_result");
+    return IPM_E_NULL;
+  }
+  FusedParams p;
+  p.x = x;
+  p.y = f == IPM_FUSED_DOT ? y : nullptr;
+  p.n = n;
+  for (int v = 0; v < 4; ++v) p.init[v] = v < nv && init ? scalar_bits(dt, (const char*)init + v * esize(dt)) : 0;
+  p.has_init = init != nullptr;
+  p.out = dev_result;
+  p.partials = (uint64_t*)((char*)ws + WS_PARTIALS);
+  p.ticket = (unsigned*)((char*)ws + WS_TICKETS);
+  const bool vec = f != IPM_FUSED_DOT || (((uintptr_t)x & 31u) == ((uintptr_t)y & 31u));
+  int grid = (int)flat_grid(dt, n);
+  if (!vec) grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid, (n + FLAT_BLOCK - 1) / FLAT_BLOCK));
+  cudaStream_t st = (cudaStream_t)stream;
+  {
+    ProfScope ps(st, 2);
+    switch (dt) {
+      case IPM_I32: FusedLaunch<IPM_I32>::launch(f, p, vec, grid, st); break;
+      case IPM_I64: FusedLaunch<IPM_I64>::launch(f, p, vec, grid, st); break;
+      case IPM_F32: FusedLaunch<IPM_F32>::launch(f, p, vec, grid, st); break;
+      case IPM_F64: FusedLaunch<IPM_F64>::launch(f, p, vec, grid, st); break;
+    }
+  }
+  CK(cudaGetLastError());
+  return IPM_OK;
+}
+
+ipm_status ipm_reduce_fused(ipm_fused f, ipm_dtype dt, const void* x, const void* y, int64_t n, void* inout,
+                            void* ws, void* stream) {
+  if (!inout) {
+    set_error("NULL inout");
+    return IPM_E_NULL;
+  }
+  void* res = (char*)ws + WS_RESULT;
+  ipm_status s = ipm_reduce_fused_async(f, dt, x, y, n, inout, res, ws, stream);
+  if (s) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaMemcpyAsync(inout, res, esize(dt) * fused_nvars(f), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
   return IPM_OK;
 }
 

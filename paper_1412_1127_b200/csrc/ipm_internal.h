@@ -10,7 +10,7 @@ namespace ipm {
 // workspace layout (bytes from the 256-aligned base); ipm_workspace_bytes() = WS_BYTES
 constexpr size_t WS_TICKETS = 0;          // uint32 tickets[WS_MAX_ROWS]
 constexpr int WS_MAX_ROWS = 1024;
-constexpr size_t WS_RESULT = 4096;        // result slot (one element, 8 bytes)
+constexpr size_t WS_RESULT = 4096;        // result slots (up to 4 elements of 8 bytes)
 constexpr size_t WS_LOCAL = 4160;         // this rank's accumulator partial (multi-GPU)
 constexpr size_t WS_ACC = 4224;           // running accumulator (host-streaming path)
 constexpr size_t WS_SLOTS = 4352;         // gathered partials, one per rank

@@ -9,6 +9,7 @@
 //                  order (deterministic) and merges the variable's original value ("merges
 //                  results across different thread blocks"; PAPER.md:205 does this on the host — see
 //                  DESIGN.md "What differs from the paper")
+//   k_2d        one scalar over a strided 2-D region (collapsed gang x vector loops)
 //   k_seg_warp  the nested gang-outer / vector-inner clause, one warp per row (a8)
 //   k_seg_tma   the same with each row staged into shared memory by TMA bulk copies (per-warp ring)
 //   k_seg_group the same for short rows: a group of G <= 32 lanes per row
@@ -87,7 +88,7 @@ struct FlatParams {
   uint64_t* partials;     // gridDim.x * gridDim.y slots (unused when gridDim.x == 1)
   unsigned* tickets;      // gridDim.y tickets (unused when gridDim.x == 1); left at zero
 };
-enum { MODE_RESULT = 0, MODE_PARTIAL = 1, MODE_ACCUM_FIRST = 2, MODE_ACCUM = 3 };
+enum { MODE_RESULT = 0, MODE_PARTIAL = 1, MODE_ACCUM_FIRST = 2, MODE_ACCUM = 3, MODE_CTA_PARTIALS = 4 };
 
 template <class R>
 __device__ __forceinline__ void store_out(const FlatParams& p, int64_t row, typename R::A total) {
@@ -123,6 +124,40 @@ __device__ __forceinline__ typename R::A block_reduce(typename R::A v, typename 
   return r;
 }
 
+// a6: publish the CTA partial of `row`; the CTA that takes the row's last ticket folds the partials in index
+// order (deterministic), merges the original value and stores; the ticket is left at zero for the next launch.
+template <class R, int BLOCK>
+__device__ __forceinline__ void grid_finish(const FlatParams& p, int64_t row, typename R::A cta, typename R::A* sm) {
+  using A = typename R::A;
+  __shared__ int s_last;
+  if (p.mode == MODE_CTA_PARTIALS) {  // the paper's first level only: one partial per thread block
+    if (threadIdx.x == 0) ((uint64_t*)p.out)[blockIdx.x] = pack(cta);
+    return;
+  }
+  if (gridDim.x == 1) {
+    if (threadIdx.x == 0) store_out<R>(p, row, cta);
+    return;
+  }
+  uint64_t* parts = p.partials + row * gridDim.x;
+  if (threadIdx.x == 0) {
+    __stcg(parts + blockIdx.x, pack(cta));
+    __threadfence();
+    const unsigned t = atomicAdd(p.tickets + row, 1u);
+    s_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  A v = R::id();
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += BLOCK) v = R::op(v, unpack<A>(__ldcg(parts + i)));
+  __syncthreads();  // sm reuse
+  A total = block_reduce<R, BLOCK>(v, sm);
+  if (threadIdx.x == 0) {
+    store_out<R>(p, row, total);
+    p.tickets[row] = 0u;
+  }
+}
+
 // ------------------------------------------------------------------------------------------ flat
 template <class R, int BLOCK, int U, int HINT = 0>
 __global__ void __launch_bounds__(BLOCK) k_flat(FlatParams p) {
@@ -132,7 +167,6 @@ __global__ void __launch_bounds__(BLOCK) k_flat(FlatParams p) {
   constexpr int VW = Vec<B>::W;
   constexpr int64_t TILE = (int64_t)BLOCK * U;
   __shared__ A sm[BLOCK / 32 > 0 ? BLOCK / 32 : 1];
-  __shared__ int s_last;
 
   const int64_t row = blockIdx.y;
   const B* a = (const B*)p.a + row * p.row_stride;
@@ -181,30 +215,72 @@ __global__ void __launch_bounds__(BLOCK) k_flat(FlatParams p) {
 
   // a4 + a5
   A cta = block_reduce<R, BLOCK>(acc[0], sm);
+  grid_finish<R, BLOCK>(p, row, cta, sm);
+}
 
-  if (gridDim.x == 1) {
-    if (threadIdx.x == 0) store_out<R>(p, row, cta);
-    return;
+// ------------------------------------------------------------------------------------------ 2-D collapse
+// One scalar over a strided 2-D region (a gang loop over rows collapsed with the
+// vector loop over columns, rows not contiguous when row_stride > cols): work items are (row, chunk of
+// 32*U vectors) pairs taken by warps in grid-stride order, so few long rows and many short rows both spread
+// over the whole GPU; each row peels its own head/tail to 32-byte alignment. Then a4-a6 as in k_flat.
+struct Params2D {
+  FlatParams f;   // f.a = base, f.n unused
+  int64_t rows, cols, row_stride;
+};
+template <class R, int BLOCK, int U>
+__global__ void __launch_bounds__(BLOCK) k_2d(Params2D q) {
+  using B = typename R::B;
+  using A = typename R::A;
+  using VT = typename Vec<B>::T;
+  constexpr int VW = Vec<B>::W;
+  constexpr int64_t CHV = 32 * U;  // vectors per work item
+  __shared__ A sm[BLOCK / 32];
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (int64_t)blockIdx.x * (BLOCK / 32) + (threadIdx.x >> 5);
+  const int64_t nw = (int64_t)gridDim.x * (BLOCK / 32);
+  // vectors per row is the same for every row only if all rows share the alignment; take the maximum
+  // (head = 0) and let rows with a head skip their last partial vector through the bounds check
+  const int64_t maxv = q.cols / VW;
+  const int64_t per_row = maxv > 0 ? (maxv + CHV - 1) / CHV : 1;
+  const int64_t items = q.rows * per_row;
+  A acc[VW];
+#pragma unroll
+  for (int k = 0; k < VW; ++k) acc[k] = R::id();
+  for (int64_t it = gw; it < items; it += nw) {
+    const int64_t r = it / per_row, c = it - r * per_row;
+    const B* a = (const B*)q.f.a + r * q.row_stride;
+    int64_t head = (int64_t)(((32u - ((uintptr_t)a & 31u)) & 31u) / sizeof(B));
+    if (head > q.cols) head = q.cols;
+    const int64_t nv = (q.cols - head) / VW;
+    const int64_t tail0 = head + nv * VW;
+    const VT* vp = (const VT*)(a + head);
+    const int64_t v0 = c * CHV + lane;
+    if (c * CHV + CHV <= nv) {
+      VT v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = ldv(vp + v0 + u * 32);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int k = 0; k < VW; ++k) acc[k] = R::op(acc[k], R::lift(v[u].w[k]));
+    } else {
+      for (int64_t i = v0; i < nv; i += 32) {
+        const VT v = ldv(vp + i);
+#pragma unroll
+        for (int k = 0; k < VW; ++k) acc[k] = R::op(acc[k], R::lift(v.w[k]));
+      }
+    }
+    if (c == 0) {
+      if (lane < head) acc[0] = R::op(acc[0], R::lift(lds(a + lane)));
+      if (lane < q.cols - tail0) acc[VW - 1] = R::op(acc[VW - 1], R::lift(lds(a + tail0 + lane)));
+    }
   }
-  // a6: publish the CTA partial; the CTA that takes the last ticket finishes the row
-  uint64_t* parts = p.partials + row * gridDim.x;
-  if (threadIdx.x == 0) {
-    __stcg(parts + blockIdx.x, pack(cta));
-    __threadfence();
-    const unsigned t = atomicAdd(p.tickets + row, 1u);
-    s_last = (t == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  A v = R::id();
-  for (int i = threadIdx.x; i < (int)gridDim.x; i += BLOCK) v = R::op(v, unpack<A>(__ldcg(parts + i)));
-  __syncthreads();  // sm reuse
-  A total = block_reduce<R, BLOCK>(v, sm);
-  if (threadIdx.x == 0) {
-    store_out<R>(p, row, total);
-    p.tickets[row] = 0u;  // ready for the next launch on this workspace
-  }
+#pragma unroll
+  for (int s = VW / 2; s > 0; s >>= 1)
+#pragma unroll
+    for (int k = 0; k < s; ++k) acc[k] = R::op(acc[k], acc[k + s]);
+  A cta = block_reduce<R, BLOCK>(acc[0], sm);
+  grid_finish<R, BLOCK>(q.f, 0, cta, sm);
 }
 
 // ------------------------------------------------------------------------------------------ segmented

@@ -58,6 +58,13 @@ def _load():
         "ipm_reduce": ([ci, ci, vp, i64, vp, vp, vp], ci),
         "ipm_reduce_async": ([ci, ci, vp, i64, vp, vp, vp, vp], ci),
         "ipm_reduce_segmented": ([ci, ci, vp, i64, i64, i64, vp, vp, vp, vp], ci),
+        "ipm_reduce_partials": ([ci, ci, vp, i64, vp, ci, ctypes.POINTER(ci), vp], ci),
+        "ipm_finalize_partials": ([ci, ci, vp, ci, vp, vp, vp], ci),
+        "ipm_reduce_2d": ([ci, ci, vp, i64, i64, i64, vp, vp, vp], ci),
+        "ipm_reduce_2d_async": ([ci, ci, vp, i64, i64, i64, vp, vp, vp, vp], ci),
+        "ipm_fused_nvars": ([ci], ci),
+        "ipm_reduce_fused": ([ci, ci, vp, vp, i64, vp, vp, vp], ci),
+        "ipm_reduce_fused_async": ([ci, ci, vp, vp, i64, vp, vp, vp, vp], ci),
         "ipm_reduce_host": ([ci, ci, vp, i64, vp, vp, vp], ci),
         "ipm_release_staging": ([], ci),
         "ipm_set_option": ([ci, i64], ci),
@@ -84,7 +91,7 @@ lib = _load()
 EXPORTED = ("ipm_status_str ipm_last_error_message ipm_op_legal ipm_dtype_size ipm_version ipm_set_allocator "
             "ipm_copyin ipm_create ipm_present ipm_update_device ipm_update_host ipm_copyout ipm_delete "
             "ipm_present_count ipm_workspace_bytes ipm_workspace_init ipm_reduce ipm_reduce_async "
-            "ipm_reduce_segmented ipm_reduce_host ipm_release_staging ipm_set_option ipm_profile_enable ipm_profile_read "
+            "ipm_reduce_segmented ipm_reduce_partials ipm_finalize_partials ipm_reduce_2d ipm_reduce_2d_async ipm_fused_nvars ipm_reduce_fused ipm_reduce_fused_async ipm_reduce_host ipm_release_staging ipm_set_option ipm_profile_enable ipm_profile_read "
             "ipm_profile_disable ipm_flat_geometry ipm_comm_id_bytes "
             "ipm_comm_unique_id ipm_comm_init ipm_comm_destroy ipm_shard_range ipm_reduce_dist "
             "ipm_reduce_dist_async").split()
@@ -229,6 +236,95 @@ def reduce_segmented(op: str, t: torch.Tensor, rows: int | None = None, cols: in
                                     None if box is None else box.ctypes.data, out.data_ptr(), ws.data_ptr(),
                                     _stream(stream)), "ipm_reduce_segmented")
     return out
+
+
+def reduce_partials(op: str, t: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """The paper's first level alone: one accumulator-typed partial per thread block (8-byte slots, returned as
+    a uint8 tensor view of int64 slots). See ipm.h for the slot format."""
+    ptr, n, dt = _flat_arg(t)
+    g, _ = flat_geometry(t.dtype, n)
+    if out is None:
+        out = torch.empty(g, dtype=torch.int64, device=t.device)
+    cnt = ctypes.c_int()
+    _check(lib.ipm_reduce_partials(op_code(op), dt, ptr, n, out.data_ptr(), out.numel(), ctypes.byref(cnt),
+                                   _stream(stream)), "ipm_reduce_partials")
+    return out[:cnt.value]
+
+
+def finalize_partials(op: str, dtype, partials: torch.Tensor, init=None, out: torch.Tensor | None = None,
+                      stream=None) -> torch.Tensor:
+    """The second level on the GPU (one warp): init ⊕ fold of the slots, in index order."""
+    dt = dtype_code(dtype)
+    if out is None:
+        out = torch.empty(1, dtype=TORCH_OF[dt], device=partials.device)
+    box = _scalar(dt, init)
+    _check(lib.ipm_finalize_partials(op_code(op), dt, partials.data_ptr(), partials.numel(),
+                                     None if box is None else box.ctypes.data, out.data_ptr(), _stream(stream)),
+           "ipm_finalize_partials")
+    return out
+
+
+def reduce_2d(op: str, t: torch.Tensor, rows: int | None = None, cols: int | None = None,
+              row_stride: int | None = None, init=None, ws: torch.Tensor | None = None, stream=None):
+    """One scalar over a strided 2-D region: init ⊕ fold_{r,j} t[r*row_stride + j] (a 2-D tensor view with
+    unit column stride works directly, e.g. ``big[:, 10:500]``). Returns a numpy scalar."""
+    if not t.is_cuda:
+        raise ValueError("expected a CUDA tensor")
+    dt = DTYPES[t.dtype]
+    if t.dim() == 2 and rows is None:
+        rows, cols = t.shape
+        row_stride = t.stride(0) if rows > 1 else cols
+        if cols > 1 and t.stride(1) != 1:
+            raise ValueError("columns must be contiguous")
+    elif rows is None or cols is None:
+        raise ValueError("rows and cols are required for a flat tensor")
+    row_stride = cols if row_stride is None else row_stride
+    ws = workspace(stream) if ws is None else ws
+    out = torch.empty(1, dtype=t.dtype, device=t.device)
+    box = _scalar(dt, init)
+    _check(lib.ipm_reduce_2d_async(op_code(op), dt, t.data_ptr(), rows, cols, row_stride,
+                                   None if box is None else box.ctypes.data, out.data_ptr(), ws.data_ptr(),
+                                   _stream(stream)), "ipm_reduce_2d_async")
+    return out.cpu().numpy()[0]
+
+
+FUSED = {"sum_sumsq": 0, "dot": 1, "minmax": 2, "stats": 3}
+
+
+def reduce_fused_async(sig: str, x: torch.Tensor, y: torch.Tensor | None = None, init=None,
+                       out: torch.Tensor | None = None, ws: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Several reduction variables in one pass (ipm_reduce_fused_async): sum_sumsq -> [Σx, Σx²], dot -> [Σxy],
+    minmax -> [min, max], stats -> [Σx, Σx², min, max]; returns a CUDA tensor of the variables."""
+    f = FUSED[sig]
+    ptr, n, dt = _flat_arg(x)
+    yp = 0
+    if f == FUSED["dot"]:
+        if y is None or y.numel() != n or y.dtype != x.dtype:
+            raise ValueError("dot needs y with the same length and dtype")
+        yp = _flat_arg(y)[0]
+    nv = lib.ipm_fused_nvars(f)
+    if out is None:
+        out = torch.empty(nv, dtype=x.dtype, device=x.device)
+    ws = workspace(stream) if ws is None else ws
+    box = None if init is None else np.ascontiguousarray(init, dtype=NP_OF[dt])
+    _check(lib.ipm_reduce_fused_async(f, dt, ptr, yp or None, n, None if box is None else box.ctypes.data,
+                                      out.data_ptr(), ws.data_ptr(), _stream(stream)), "ipm_reduce_fused_async")
+    return out
+
+
+def reduce_fused(sig: str, x: torch.Tensor, y: torch.Tensor | None = None, init=None,
+                 ws: torch.Tensor | None = None, stream=None) -> np.ndarray:
+    """Blocking form: returns the variables as a numpy array (init: one value per variable, or None)."""
+    if init is None:
+        return reduce_fused_async(sig, x, y, None, ws=ws, stream=stream).cpu().numpy()
+    f = FUSED[sig]
+    ptr, n, dt = _flat_arg(x)
+    yp = _flat_arg(y)[0] if f == FUSED["dot"] else None
+    box = np.array(init, dtype=NP_OF[dt]).copy()
+    ws = workspace(stream) if ws is None else ws
+    _check(lib.ipm_reduce_fused(f, dt, ptr, yp, n, box.ctypes.data, ws.data_ptr(), _stream(stream)),
+           "ipm_reduce_fused")
+    return box
 
 
 def reduce_host(op: str, a, init=None, ws: torch.Tensor | None = None, stream=None):

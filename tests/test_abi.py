@@ -20,14 +20,14 @@ def ipm():
 def header_functions():
     src = open(os.path.join(ROOT, "include", "ipm.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(ipm_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(ipm_[a-z_0-9]+)\s*\(", src)))
 
 
 def test_exports_every_declared_symbol(ipm):
     names = header_functions()
     assert len(names) >= 28
     nm = os.popen(f"nm -D --defined-only {ipm.LIB_PATH}").read()
-    exported = set(re.findall(r"\bT (ipm_[a-z_]+)", nm))
+    exported = set(re.findall(r"\bT (ipm_[a-z_0-9]+)", nm))
     missing = [n for n in names if n not in exported]
     assert not missing, missing
     assert set(ipm.EXPORTED) == set(names)

@@ -282,3 +282,63 @@ def test_dist_world1(ipm):
         want_t, want_ld = oracle.reduce(op, ipmgen.fill_host(spec), init=NPT[dt](1))
         check(op, dt, got, want_t, want_ld)
     comm.close()
+
+
+# --------------------------------------------------------------------------- several variables, one pass
+
+FSIGS = ["sum_sumsq", "dot", "minmax", "stats"]
+
+
+@pytest.mark.parametrize("dt", DTS)
+@pytest.mark.parametrize("sig", FSIGS)
+def test_fused_parity(ipm, sig, dt):
+    for i, n in enumerate([0, 1, 5, 33, 1000, 4097, 65_537, (1 << 20) + 3]):
+        kind = "signed" if sig in ("minmax", "stats") else "random"
+        sx = ipmgen.Spec(dt, n, kind, seed=i + 1)
+        sy = ipmgen.Spec(dt, n, kind, seed=i + 101)
+        for offx, offy in [(0, 0), (i % 8, i % 8), (1, 2)]:    # same and different alignment (DOT)
+            x = device_input(sx, offx)
+            y = device_input(sy, offy)
+            nv = {"sum_sumsq": 2, "dot": 1, "minmax": 2, "stats": 4}[sig]
+            init = np.arange(1, nv + 1).astype(NPT[dt])
+            got = ipm.reduce_fused(sig, x, y if sig == "dot" else None, init=init)
+            want_t, want_ld = oracle.reduce_fused(sig, ipmgen.fill_host(sx),
+                                                  ipmgen.fill_host(sy) if sig == "dot" else None, init=init)
+            ops = {"sum_sumsq": ["+", "+"], "dot": ["+"], "minmax": ["min", "max"],
+                   "stats": ["+", "+", "min", "max"]}[sig]
+            for v, op in enumerate(ops):
+                check(op, dt, got[v], want_t[v], want_ld[v])
+
+
+def test_fused_srad_statistics_closed_form(ipm):
+    # SRAD-style image statistics: a_i = i mod 1024 -> Σ and Σ² in closed form, exact
+    n = 1 << 24
+    x = torch.arange(n, device="cuda", dtype=torch.int64).remainder(1024).to(torch.float32)
+    s, s2, lo, hi = ipm.reduce_fused("stats", x)
+    k = n // 1024
+    assert s == k * 523776 and s2 == k * sum(i * i for i in range(1024)) and lo == 0 and hi == 1023
+
+
+# --------------------------------------------------------------------------- strided 2-D region -> one scalar
+
+@pytest.mark.parametrize("op,dt", LEGAL)
+def test_2d_collapse_parity(ipm, op, dt):
+    shapes = [(0, 5, 5), (3, 0, 4), (1, 1, 1), (7, 3, 5), (100, 33, 40), (5, 5000, 5003), (3, 300_001, 300_010),
+              (2000, 257, 300), (64, 4096, 4096), (4096, 1, 3)]
+    for k, (rows, cols, stride) in enumerate(shapes):
+        total = max(0, (rows - 1) * stride + cols) if rows else 0
+        spec = workload(op, dt, total, seed=k + 3)
+        x = device_input(spec, offset=k % 8)
+        init = NPT[dt](2)
+        got = ipm.reduce_2d(op, x, rows=rows, cols=cols, row_stride=stride, init=init)
+        h = ipmgen.fill_host(spec)
+        region = np.concatenate([h[r * stride:r * stride + cols] for r in range(rows)]) if rows and cols else h[:0]
+        want_t, want_ld = oracle.reduce(op, region, init=init)   # the plain fold over the region, row-major
+        check(op, dt, got, want_t, want_ld)
+
+
+def test_2d_view_api(ipm):
+    big = torch.arange(1000 * 700, dtype=torch.int64, device="cuda").view(1000, 700)
+    sub = big[10:900, 33:650]
+    assert ipm.reduce_2d("+", sub) == int(sub.sum())
+    assert ipm.reduce_2d("max", sub) == int(sub.max())
