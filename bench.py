@@ -235,6 +235,28 @@ def suite(ipm, torch, ipmgen, peak):
             gbs = x.numel() * x.element_size() / med / 1e6
             out[f"C4_{dt}_{op}_2^30"] = {"kernel_ms_median": med, "GB/s": gbs, "frac": gbs / peak}
         del x
+    # NEXT rows: several variables in one pass (SRAD statistics, dot) and a strided 2-D region
+    n = 1 << 28
+    x = torch.empty(n, dtype=torch.float32, device="cuda")
+    ipmgen.fill_tensor(ipmgen.Spec("float32", n, "random", seed=1), x)
+    y = torch.empty(n, dtype=torch.float32, device="cuda")
+    ipmgen.fill_tensor(ipmgen.Spec("float32", n, "random", seed=2), y)
+    r = torch.empty(4, dtype=torch.float32, device="cuda")
+    for sig, nbytes in (("stats", n * 4), ("dot", 2 * n * 4)):
+        ms = timed(lambda: ipm.reduce_fused_async(sig, x, y if sig == "dot" else None, out=r, ws=ws))
+        med = statistics.median(ms)
+        out[f"fused_{sig}_float32_2^28"] = {"kernel_ms_median": med, "GB/s": nbytes / med / 1e6,
+                                            "frac": nbytes / med / 1e6 / peak}
+    del y
+    rows, cols, stride = 16384, 16000, 16384  # a 16384 x 16000 window of a 16384 x 16384 float32 image
+    x2 = x[: rows * stride]
+    r1 = torch.empty(1, dtype=torch.float32, device="cuda")
+    ms = timed(lambda: ipm.lib.ipm_reduce_2d_async(0, 2, x2.data_ptr(), rows, cols, stride, None, r1.data_ptr(),
+                                                   ws.data_ptr(), torch.cuda.current_stream().cuda_stream))
+    med = statistics.median(ms)
+    out["2d_float32_16384x16000_stride16384"] = {"kernel_ms_median": med, "GB/s": rows * cols * 4 / med / 1e6,
+                                                 "frac": rows * cols * 4 / med / 1e6 / peak}
+    del x, x2
     torch.cuda.empty_cache()
     return out
 

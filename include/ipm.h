@@ -181,6 +181,17 @@ ipm_status ipm_reduce_fused(ipm_fused f, ipm_dtype dt, const void* x, const void
 ipm_status ipm_reduce_fused_async(ipm_fused f, ipm_dtype dt, const void* x, const void* y, int64_t n,
                                   const void* init, void* dev_result, void* workspace, void* stream);
 
+/* Ragged nested clause: an outer gang loop over rows whose inner vector loop has
+ * data-dependent bounds — BFS's adjacency loops — given in CSR form:
+ *   for r in [0, rows): dev_out[r] = init ⊕ fold_{j = off[r] .. off[r+1]-1} dev[j]
+ * dev_offsets: device array of rows+1 int64 element indices, non-decreasing (off[0] need not be 0; results are
+ * undefined otherwise). dev: the element array (indices off[0] .. off[rows]-1 are read). dev_out: rows
+ * elements. Work is balanced by elements, not rows: rows of any length, including a few huge ones, spread over
+ * all SMs; rows split between warps are finished by a second one-warp-per-split kernel, folding the pieces in
+ * order (deterministic). Two kernel launches; workspace required. */
+ipm_status ipm_reduce_ragged(ipm_op op, ipm_dtype dt, const void* dev, const int64_t* dev_offsets, int64_t rows,
+                             const void* init, void* dev_out, void* workspace, void* stream);
+
 /* End-to-end clause over a HOST array: the data clause `copyin(a[0:n])` fused with the reduction. The host
  * array is streamed to the device in chunks through two library-owned staging buffers (allocated once
  * through the allocator hook and kept until ipm_release_staging), each chunk's H2D copy overlapping the
@@ -204,8 +215,12 @@ ipm_status ipm_profile_disable(void);
  *   IPM_OPT_FLAT_CTAS_PER_SM  CTAs per SM of the flat kernel's persistent grid, 1..8 (-1 = default 4)
  *   IPM_OPT_SEG_KERNEL        segmented rows: 0 auto (direct 256-bit loads), 1 direct loads, 2 TMA bulk copies
  *                             into a per-warp shared-memory ring (rows of >= 64 bytes)
+ *   IPM_OPT_DETERMINISTIC     1 (default): float + and * of the flat clause use a static tile schedule, so
+ *                             repeated runs give identical bits; 0: every op takes tiles dynamically (faster
+ *                             on some sizes; float results may then differ in the last bits between runs).
+ *                             Exact operators always use the dynamic schedule.
  * IPM_E_ARG for an unknown key or an out-of-range value. */
-typedef enum { IPM_OPT_FLAT_CTAS_PER_SM = 0, IPM_OPT_SEG_KERNEL = 1 } ipm_option;
+typedef enum { IPM_OPT_FLAT_CTAS_PER_SM = 0, IPM_OPT_SEG_KERNEL = 1, IPM_OPT_DETERMINISTIC = 2 } ipm_option;
 ipm_status ipm_set_option(ipm_option key, int64_t value);
 
 /* Launch geometry the library uses for a flat reduce of n elements (for tests and the roofline report). */

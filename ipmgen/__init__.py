@@ -113,3 +113,46 @@ def fill_tensor(spec: Spec, t, lo: int = 0) -> None:
     """Fill a contiguous CUDA torch tensor with elements [lo, lo+t.numel())."""
     import torch
     fill_device(spec, t.data_ptr(), lo, t.numel(), torch.cuda.current_stream(t.device).cuda_stream)
+
+
+DEGREE_TAG = 0xD1B54A32D192ED03
+
+
+def draws(seed: int, idx: np.ndarray) -> np.ndarray:
+    """Vectorised h(seed, i) for an array of indices (the same splitmix64 stream as ipmgen.h; tests compare it
+    with the C implementation)."""
+    G = np.uint64(0x9E3779B97F4A7C15)
+    with np.errstate(over="ignore"):
+        z = np.uint64(seed & (2**64 - 1)) * G + (idx.astype(np.uint64) + np.uint64(1)) * G
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return z ^ (z >> np.uint64(31))
+
+
+def degrees(rows: int, seed: int = 1, kind: str = "powerlaw", mean: float = 16.0, alpha: float = 1.5,
+            cap: int | None = None) -> np.ndarray:
+    """Row lengths of a ragged (CSR) input — graph adjacency lists for the BFS-style nested loop.
+    powerlaw: d = floor(dmin * u^(-1/alpha)) with u uniform in (0,1] from h(seed ^ TAG, r), dmin chosen so the mean
+    is about `mean`, capped at `cap`; uniform: d in [0, 2*mean]; const: d = mean."""
+    r = np.arange(rows, dtype=np.uint64)
+    if kind == "const":
+        return np.full(rows, int(mean), dtype=np.int64)
+    z = draws(seed ^ DEGREE_TAG, r)
+    u = ((z >> np.uint64(11)).astype(np.float64) + 1.0) * 2.0 ** -53          # (0, 1]
+    if kind == "uniform":
+        d = np.floor(u * (2 * mean + 1)).astype(np.int64)
+        d = np.minimum(d, int(2 * mean))
+    else:
+        dmin = mean * (alpha - 1) / alpha
+        d = np.floor(dmin * u ** (-1.0 / alpha)).astype(np.int64)
+    if cap is not None:
+        d = np.minimum(d, cap)
+    return d
+
+
+def offsets_from_degrees(d: np.ndarray, start: int = 0) -> np.ndarray:
+    off = np.empty(d.size + 1, dtype=np.int64)
+    off[0] = start
+    np.cumsum(d, out=off[1:])
+    off[1:] += start
+    return off

@@ -44,6 +44,8 @@ def lib():
         L.ora_reduce.restype = ci
         L.ora_reduce_segmented.argtypes = [ci, ci, vp, i64, i64, i64, vp, vp, vp]
         L.ora_reduce_segmented.restype = ci
+        L.ora_reduce_ragged.argtypes = [ci, ci, vp, vp, i64, vp, vp, vp]
+        L.ora_reduce_ragged.restype = ci
         L.ora_fused_nvars.argtypes = [ci]
         L.ora_fused_nvars.restype = ci
         L.ora_reduce_fused.argtypes = [ci, ci, vp, vp, i64, vp, vp, vp]
@@ -148,4 +150,22 @@ def reduce_fused(sig: str, x, y=None, dtype: str | None = None, init=None):
                                 None if ib is None else ib.ctypes.data, out.ctypes.data, out_ld.ctypes.data)
     if rc:
         raise ValueError(f"ora_reduce_fused failed ({rc})")
+    return out, out_ld
+
+
+def reduce_ragged(op: str, a, offsets, dtype: str | None = None, init=None):
+    """out[r] = init ⊕ fold a[offsets[r]:offsets[r+1]]; returns (out as T array, long double array)."""
+    a = np.ascontiguousarray(a)
+    dtype = dtype or a.dtype.name
+    a = a.astype(NP[dtype], copy=False)
+    off = np.ascontiguousarray(offsets, dtype=np.int64)
+    rows = off.size - 1
+    out = np.zeros(max(rows, 0), dtype=NP[dtype])
+    out_ld = np.zeros(max(rows, 0), dtype=np.longdouble)
+    ib = _scalar_buf(dtype, init)
+    rc = lib().ora_reduce_ragged(OPS[op], DTYPES[dtype], a.ctypes.data if a.size else None, off.ctypes.data, rows,
+                                 None if ib is None else ib.ctypes.data, out.ctypes.data if rows else None,
+                                 out_ld.ctypes.data if rows else None)
+    if rc:
+        raise ValueError(f"ora_reduce_ragged failed ({rc})")
     return out, out_ld

@@ -271,3 +271,21 @@ int ora_reduce_fused(int f, int dt, const void* x, const void* y, int64_t n, con
     ora_result(&st[v], out ? (char*)out + v * es : 0, out_ld ? out_ld + v : 0);
   return 0;
 }
+
+/* ragged (CSR) nested clause (BFS-style inner loops with data-dependent bounds,
+ * PAPER.md:175-177): out[r] = init ⊕ fold_{j = offsets[r] .. offsets[r+1]-1} a[j], each row an independent
+ * left fold in index order. offsets: rows+1 non-decreasing int64 element indices into a. */
+int ora_reduce_ragged(int op, int dt, const void* a, const int64_t* offsets, int64_t rows, const void* init,
+                      void* out, long double* out_ld) {
+  if (!ora_legal(op, dt)) return 1;
+  if (rows < 0) return 2;
+  const int es = (dt == T_I32 || dt == T_F32) ? 4 : 8;
+  for (int64_t r = 0; r < rows; ++r) {
+    if (offsets[r + 1] < offsets[r]) return 3;
+    ora_state st;
+    ora_begin(&st, op, dt, init);
+    for (int64_t j = offsets[r]; j < offsets[r + 1]; ++j) step(&st, a, j);
+    ora_result(&st, out ? (char*)out + (size_t)r * es : 0, out_ld ? out_ld + r : 0);
+  }
+  return 0;
+}

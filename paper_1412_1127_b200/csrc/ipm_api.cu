@@ -54,6 +54,7 @@ constexpr int FLAT_U = 4;  // 4 x 32 B in flight per thread
 // run-time options (ipm_set_option); defaults chosen by tools/sweep_flat.cu measurements
 static int g_opt_flat_cps = -1;  // CTAs per SM for k_flat (-1: IPM_CTAS_PER_SM env or 4)
 static int g_opt_seg_kernel = 0; // 0 auto, 1 k_seg_warp (LDG), 2 k_seg_tma (bulk copies)
+static int g_opt_deterministic = 1;  // 1: float + and * keep a static schedule (bit-reproducible)
 static int flat_ctas_per_sm() {
   if (g_opt_flat_cps > 0) return g_opt_flat_cps;
   static int v = std::max(1, std::min(8, env_int("IPM_CTAS_PER_SM", 4)));
@@ -151,11 +152,23 @@ static void prof_free() {
 template <int OP, int DT>
 struct Launch {
   using R = Red<OP, DT>;
+  // exact operators (every result bit independent of the grouping) take tiles dynamically from an atomic
+  // counter, which absorbs per-SM bandwidth differences (tools/sweep_flat.cu: +2% at 16 GiB, +11% at 1 GiB);
+  // float + and * keep the static grid-stride schedule so that their rounding, hence their bits, are the
+  // same on every run (IPM_OPT_DETERMINISTIC, default 1).
+  static constexpr bool kExact = !((DT == IPM_F32 || DT == IPM_F64) && (OP == IPM_ADD || OP == IPM_MUL));
   static void flat(const FlatParams& p, dim3 grid, cudaStream_t st) {
-    k_flat<R, FLAT_BLOCK, FLAT_U><<<grid, FLAT_BLOCK, 0, st>>>(p);
+    if (p.counter && grid.y == 1 && (kExact || !g_opt_deterministic))
+      k_flat<R, FLAT_BLOCK, FLAT_U, 0, 2><<<grid, FLAT_BLOCK, 0, st>>>(p);
+    else
+      k_flat<R, FLAT_BLOCK, FLAT_U, 0, 0><<<grid, FLAT_BLOCK, 0, st>>>(p);
   }
   static void seg_warp(const SegParams& p, int grid, cudaStream_t st) {
     k_seg_warp<R, SEG_WARPS, SEG_U><<<grid, SEG_WARPS * 32, 0, st>>>(p);
+  }
+  static void ragged(const RaggedParams& p, int blocks, int64_t nw, cudaStream_t st) {
+    k_ragged<R, 8><<<blocks, 256, 0, st>>>(p);
+    k_ragged_fix<R><<<(unsigned)((nw + 7) / 8), 256, 0, st>>>(p, nw);
   }
   static void two_d(const Params2D& q, int grid, cudaStream_t st) {
     k_2d<R, FLAT_BLOCK, 4><<<grid, FLAT_BLOCK, 0, st>>>(q);
@@ -185,6 +198,7 @@ struct Launch {
 struct Table {
   void (*flat)(const FlatParams&, dim3, cudaStream_t);
   void (*two_d)(const Params2D&, int, cudaStream_t);
+  void (*ragged)(const RaggedParams&, int, int64_t, cudaStream_t);
   void (*seg_warp)(const SegParams&, int, cudaStream_t);
   cudaError_t (*seg_tma)(const SegParams&, int, cudaStream_t);
   void (*seg_group)(const SegParams&, int, int, cudaStream_t);
@@ -194,7 +208,7 @@ struct Table {
 static const Table* table(ipm_op op, ipm_dtype dt) {
 #define IPM_ENTRY(O, D)                                                                                  \
   if (op == O && dt == D) {                                                                            \
-    static const Table t = {&Launch<O, D>::flat, &Launch<O, D>::two_d, &Launch<O, D>::seg_warp, &Launch<O, D>::seg_tma,     \
+    static const Table t = {&Launch<O, D>::flat, &Launch<O, D>::two_d, &Launch<O, D>::ragged, &Launch<O, D>::seg_warp, &Launch<O, D>::seg_tma,     \
                             &Launch<O, D>::seg_group, &Launch<O, D>::finalize};                        \
     return &t;                                                                                         \
   }
@@ -240,6 +254,7 @@ ipm_status launch_flat(ipm_op op, ipm_dtype dt, const void* dev, int64_t n, uint
   p.out = out;
   p.partials = (uint64_t*)((char*)ws + WS_PARTIALS);
   p.tickets = (unsigned*)((char*)ws + WS_TICKETS);
+  p.counter = (unsigned long long*)((char*)ws + WS_COUNTER);
   {
     ProfScope ps(st, 0);
     t->flat(p, dim3((unsigned)flat_grid(dt, n), 1, 1), st);
@@ -410,6 +425,10 @@ ipm_status ipm_set_option(ipm_option key, int64_t value) {
       if (value < 0 || value > 2) break;
       g_opt_seg_kernel = (int)value;
       return IPM_OK;
+    case IPM_OPT_DETERMINISTIC:
+      if (value < 0 || value > 1) break;
+      g_opt_deterministic = (int)value;
+      return IPM_OK;
   }
   set_error("unknown option or value out of range");
   return IPM_E_ARG;
@@ -540,6 +559,7 @@ ipm_status ipm_reduce_segmented(ipm_op op, ipm_dtype dt, const void* dev, int64_
     p.out = dev_out;
     p.partials = ws ? (uint64_t*)((char*)ws + WS_PARTIALS) : nullptr;
     p.tickets = ws ? (unsigned*)((char*)ws + WS_TICKETS) : nullptr;
+    p.counter = nullptr;
     {
       ProfScope ps(st, 1);
       t->flat(p, dim3((unsigned)S, (unsigned)rows, 1), st);
@@ -598,6 +618,7 @@ ipm_status ipm_reduce_partials(ipm_op op, ipm_dtype dt, const void* dev, int64_t
   p.out = dev_partials;
   p.partials = nullptr;
   p.tickets = nullptr;
+  p.counter = nullptr;
   cudaStream_t st = (cudaStream_t)stream;
   {
     ProfScope ps(st, 0);
@@ -622,6 +643,46 @@ ipm_status ipm_finalize_partials(ipm_op op, ipm_dtype dt, const void* dev_partia
   }
   return launch_finalize(op, dt, (const uint64_t*)dev_partials, count, scalar_bits(dt, init), init != nullptr,
                          dev_result, (cudaStream_t)stream);
+}
+
+// ---------------------------------------------------------------------------------- ragged rows
+ipm_status ipm_reduce_ragged(ipm_op op, ipm_dtype dt, const void* dev, const int64_t* dev_offsets, int64_t rows,
+                             const void* init, void* dev_out, void* ws, void* stream) {
+  ipm_status s;
+  if ((s = validate(op, dt)) || (s = check_ws(ws))) return s;
+  if (rows < 0) {
+    set_error("negative row count");
+    return IPM_E_SIZE;
+  }
+  if (rows == 0) return IPM_OK;
+  if (!dev_offsets || !dev_out) {
+    set_error("NULL device pointer");
+    return IPM_E_NULL;
+  }
+  if (((uintptr_t)dev_out % esize(dt)) || (dev && ((uintptr_t)dev % esize(dt))) || ((uintptr_t)dev_offsets & 7u)) {
+    set_error("device pointer not aligned to its element size");
+    return IPM_E_ALIGN;
+  }
+  RaggedParams p;
+  p.a = dev;
+  p.off = dev_offsets;
+  p.rows = rows;
+  p.init = scalar_bits(dt, init);
+  p.has_init = init != nullptr;
+  p.out = dev_out;
+  const int64_t nw = std::min<int64_t>((int64_t)sm_count() * 32, WS_MAX_RAGGED_WARPS);
+  int64_t* base = (int64_t*)((char*)ws + WS_RAGGED);
+  p.head_row = base;
+  p.head_part = (uint64_t*)(base + WS_MAX_RAGGED_WARPS);
+  p.tail_row = base + 2 * WS_MAX_RAGGED_WARPS;
+  p.tail_part = (uint64_t*)(base + 3 * WS_MAX_RAGGED_WARPS);
+  cudaStream_t st = (cudaStream_t)stream;
+  {
+    ProfScope ps(st, 4);
+    table(op, dt)->ragged(p, (int)(nw / 8), nw, st);
+  }
+  CK(cudaGetLastError());
+  return IPM_OK;
 }
 
 // ---------------------------------------------------------------------------------- 2-D collapse
@@ -664,6 +725,7 @@ ipm_status ipm_reduce_2d_async(ipm_op op, ipm_dtype dt, const void* dev, int64_t
   q.f.out = dev_result;
   q.f.partials = (uint64_t*)((char*)ws + WS_PARTIALS);
   q.f.tickets = (unsigned*)((char*)ws + WS_TICKETS);
+  q.f.counter = nullptr;
   q.rows = rows;
   q.cols = cols;
   q.row_stride = row_stride;

@@ -13,11 +13,14 @@ constexpr int WS_MAX_ROWS = 1024;
 constexpr size_t WS_RESULT = 4096;        // result slots (up to 4 elements of 8 bytes)
 constexpr size_t WS_LOCAL = 4160;         // this rank's accumulator partial (multi-GPU)
 constexpr size_t WS_ACC = 4224;           // running accumulator (host-streaming path)
+constexpr size_t WS_COUNTER = 4288;       // dynamic tile counter of the flat kernel (left at zero)
 constexpr size_t WS_SLOTS = 4352;         // gathered partials, one per rank
 constexpr int WS_MAX_RANKS = 64;
 constexpr size_t WS_PARTIALS = 8192;      // per-CTA partials
 constexpr int WS_MAX_PARTIALS = 16384;
-constexpr size_t WS_BYTES = WS_PARTIALS + 8 * (size_t)WS_MAX_PARTIALS;
+constexpr size_t WS_RAGGED = WS_PARTIALS + 8 * (size_t)WS_MAX_PARTIALS;  // ragged head/tail records
+constexpr int WS_MAX_RAGGED_WARPS = 8192;
+constexpr size_t WS_BYTES = WS_RAGGED + 4 * 8 * (size_t)WS_MAX_RAGGED_WARPS;
 
 // error plumbing: thread-local detail string for ipm_last_error_message()
 void set_error(const std::string& msg);

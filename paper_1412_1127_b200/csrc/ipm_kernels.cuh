@@ -87,6 +87,7 @@ struct FlatParams {
   void* out;
   uint64_t* partials;     // gridDim.x * gridDim.y slots (unused when gridDim.x == 1)
   unsigned* tickets;      // gridDim.y tickets (unused when gridDim.x == 1); left at zero
+  unsigned long long* counter;  // SCHED 2 only: dynamic tile counter, left at zero
 };
 enum { MODE_RESULT = 0, MODE_PARTIAL = 1, MODE_ACCUM_FIRST = 2, MODE_ACCUM = 3, MODE_CTA_PARTIALS = 4 };
 
@@ -135,7 +136,10 @@ __device__ __forceinline__ void grid_finish(const FlatParams& p, int64_t row, ty
     return;
   }
   if (gridDim.x == 1) {
-    if (threadIdx.x == 0) store_out<R>(p, row, cta);
+    if (threadIdx.x == 0) {
+      store_out<R>(p, row, cta);
+      if (p.counter) *p.counter = 0ull;  // (the single CTA has finished claiming tiles)
+    }
     return;
   }
   uint64_t* parts = p.partials + row * gridDim.x;
@@ -155,11 +159,15 @@ __device__ __forceinline__ void grid_finish(const FlatParams& p, int64_t row, ty
   if (threadIdx.x == 0) {
     store_out<R>(p, row, total);
     p.tickets[row] = 0u;
+    if (p.counter) *p.counter = 0ull;
   }
 }
 
 // ------------------------------------------------------------------------------------------ flat
-template <class R, int BLOCK, int U, int HINT = 0>
+// SCHED: how whole tiles are assigned to CTAs — 0 grid-stride (static, interleaved), 1 one contiguous balanced
+// range per CTA, 2 dynamic (an atomic tile counter; absorbs per-SM bandwidth differences). tools/sweep_flat.cu
+// measures them.
+template <class R, int BLOCK, int U, int HINT = 0, int SCHED = 0>
 __global__ void __launch_bounds__(BLOCK) k_flat(FlatParams p) {
   using B = typename R::B;
   using A = typename R::A;
@@ -185,7 +193,7 @@ __global__ void __launch_bounds__(BLOCK) k_flat(FlatParams p) {
 
   // a3: the hot loop — whole tiles of BLOCK*U vectors, U independent 256-bit loads in flight per thread
   const int64_t ntiles = nv / TILE;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+  auto tile = [&](int64_t t) {
     const VT* base = vp + t * TILE + threadIdx.x;
     VT v[U];
 #pragma unroll
@@ -194,6 +202,22 @@ __global__ void __launch_bounds__(BLOCK) k_flat(FlatParams p) {
     for (int u = 0; u < U; ++u)
 #pragma unroll
       for (int k = 0; k < VW; ++k) acc[k] = R::op(acc[k], R::lift(v[u].w[k]));
+  };
+  if (SCHED == 0) {
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) tile(t);
+  } else if (SCHED == 1) {
+    const int64_t t1 = (ntiles * (blockIdx.x + 1)) / gridDim.x;
+    for (int64_t t = (ntiles * blockIdx.x) / gridDim.x; t < t1; ++t) tile(t);
+  } else {
+    __shared__ long long s_next;
+    int64_t t = blockIdx.x;
+    while (t < ntiles) {
+      if (threadIdx.x == 0) s_next = (long long)atomicAdd(p.counter, 1ull) + gridDim.x;
+      tile(t);
+      __syncthreads();
+      t = s_next;
+      __syncthreads();
+    }
   }
   // ragged last tile
   for (int64_t i = ntiles * TILE + (int64_t)blockIdx.x * BLOCK + threadIdx.x; i < nv;
@@ -511,6 +535,172 @@ __global__ void __launch_bounds__(32) k_finalize(const uint64_t* slots, int P, u
   if (threadIdx.x == 0) {
     if (has_init) v = R::op(R::lift((B)init), v);
     *(B*)out = R::fin(v);
+  }
+}
+
+}  // namespace ipm
+
+namespace ipm {
+
+// ------------------------------------------------------------------------------------------ ragged (CSR)
+// out[r] = init ⊕ fold a[off[r] .. off[r+1]) for rows with data-dependent lengths (SURVEY.md §8(f) rank 2:
+// BFS-style adjacency loops). Load balance by ELEMENTS, not rows: warp w of nw owns the
+// element range [lo, hi) = [P0 + w*nnz/nw, P0 + (w+1)*nnz/nw) and every row whose first element (off[r]) lies in
+// it. A row that ends inside its owner's range is finished by the owner; a row that runs past hi leaves a
+// TAIL record (row, owner's partial) and every later warp whose range it covers leaves a HEAD record; a second
+// one-warp-per-record kernel folds tail + heads in warp order (deterministic) and finishes those rows.
+struct RaggedParams {
+  const void* a;
+  const int64_t* off;     // rows + 1 offsets
+  int64_t rows;
+  uint64_t init;
+  int has_init;
+  void* out;
+  int64_t* head_row;      // per warp: the row continued from the previous warp (-1: none)
+  uint64_t* head_part;
+  int64_t* tail_row;      // per warp: the owned row that continues into the next warp (-1: none)
+  uint64_t* tail_part;
+};
+
+// first index r in [0, rows] with off[r] >= x (off non-decreasing); 32-ary search by the whole warp
+__device__ __forceinline__ int64_t warp_lower_bound(const int64_t* off, int64_t rows, int64_t x) {
+  const int lane = threadIdx.x & 31;
+  int64_t lo = 0, hi = rows;  // answer in [lo, hi]
+  while (hi - lo > 32) {
+    const int64_t step = (hi - lo + 31) / 32;
+    const int64_t idx = min(lo + (int64_t)lane * step, hi);
+    const unsigned ge = __ballot_sync(FULL, __ldg(off + idx) >= x);
+    // lanes are increasing in idx: the first lane with off >= x bounds the answer from above
+    const int f = ge ? __ffs(ge) - 1 : 32;
+    const int64_t nhi = f < 32 ? min(lo + (int64_t)f * step, hi) : hi;
+    const int64_t nlo = f > 0 ? min(lo + (int64_t)(f - 1) * step, hi) + 1 : lo;
+    lo = nlo;
+    hi = nhi;
+  }
+  const int64_t idx = lo + lane;
+  const unsigned ge = __ballot_sync(FULL, idx <= hi && __ldg(off + min(idx, hi)) >= x);
+  return ge ? lo + (__ffs(ge) - 1) : hi;
+}
+
+// the lanes' private fold of a[s..e) (not yet combined across lanes)
+template <class R>
+__device__ __forceinline__ typename R::A warp_fold_range(const typename R::B* a, int64_t s, int64_t e) {
+  using B = typename R::B;
+  using A = typename R::A;
+  using VT = typename Vec<B>::T;
+  constexpr int VW = Vec<B>::W;
+  const int lane = threadIdx.x & 31;
+  A acc = R::id();
+  if (e - s >= 4 * 32 * VW) {  // long segment: 32-byte vectors with a head/tail peel
+    const B* p = a + s;
+    int64_t head = (int64_t)(((32u - ((uintptr_t)p & 31u)) & 31u) / sizeof(B));
+    const int64_t n = e - s;
+    const int64_t nv = (n - head) / VW;
+    const int64_t tail0 = head + nv * VW;
+    const VT* vp = (const VT*)(p + head);
+    A v2[2] = {R::id(), R::id()};
+    int64_t i = lane;
+    for (; i + 32 < nv; i += 64) {
+      const VT x0 = ldv(vp + i), x1 = ldv(vp + i + 32);
+#pragma unroll
+      for (int k = 0; k < VW; ++k) {
+        v2[0] = R::op(v2[0], R::lift(x0.w[k]));
+        v2[1] = R::op(v2[1], R::lift(x1.w[k]));
+      }
+    }
+    for (; i < nv; i += 32) {
+      const VT x0 = ldv(vp + i);
+#pragma unroll
+      for (int k = 0; k < VW; ++k) v2[0] = R::op(v2[0], R::lift(x0.w[k]));
+    }
+    if (lane < head) v2[1] = R::op(v2[1], R::lift(lds(p + lane)));
+    if (lane < n - tail0) v2[1] = R::op(v2[1], R::lift(lds(p + tail0 + lane)));
+    acc = R::op(v2[0], v2[1]);
+  } else {
+    for (int64_t j = s + lane; j < e; j += 32) acc = R::op(acc, R::lift(lds(a + j)));
+  }
+  return acc;
+}
+
+template <class R, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_ragged(RaggedParams p) {
+  using B = typename R::B;
+  using A = typename R::A;
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5);
+  const int64_t nw = (int64_t)gridDim.x * WARPS;
+  const B* a = (const B*)p.a;
+  const int64_t P0 = __ldg(p.off), P1 = __ldg(p.off + p.rows);
+  const int64_t nnz = P1 - P0;
+  const int64_t lo = P0 + (int64_t)(((__int128)nnz * w) / nw);
+  const int64_t hi = P0 + (int64_t)(((__int128)nnz * (w + 1)) / nw);
+  const bool last = (w == nw - 1);
+  int64_t r = warp_lower_bound(p.off, p.rows, lo);  // first row starting at or after lo
+  // head: the row that started before lo and still has elements at lo (-2: this warp's range is empty and
+  // transparent to the fix-up walk, which happens when nnz < nw)
+  int64_t hrow = lo < hi ? -1 : -2;
+  A hpart = R::id();
+  if (r > 0 && lo < hi) {
+    const int64_t prev_end = r <= p.rows ? __ldg(p.off + r) : P1;
+    if (__ldg(p.off + r - 1) < lo && prev_end > lo) {
+      hrow = r - 1;
+      hpart = R::warp(warp_fold_range<R>(a, lo, min(prev_end, hi)));
+    }
+  }
+  // owned rows: off[r] in [lo, hi) (the last warp also owns the empty rows that start at P1)
+  int64_t trow = -1;
+  A tpart = R::id();
+  while (r < p.rows) {
+    const int64_t s = __ldg(p.off + r);
+    if (!(s < hi || (last && s == P1))) break;
+    const int64_t e = __ldg(p.off + r + 1);
+    A t = R::warp(warp_fold_range<R>(a, s, min(e, hi)));
+    if (e <= hi) {
+      if (lane == 0) {
+        if (p.has_init) t = R::op(R::lift((B)p.init), t);
+        ((B*)p.out)[r] = R::fin(t);
+      }
+    } else {
+      trow = r;
+      tpart = t;
+      break;  // a row running past hi is the last row this warp owns
+    }
+    ++r;
+  }
+  if (lane == 0) {
+    p.head_row[w] = hrow;
+    p.head_part[w] = pack(hpart);
+    p.tail_row[w] = trow;
+    p.tail_part[w] = pack(tpart);
+  }
+}
+
+// one warp per phase-1 warp: a warp with a TAIL record finishes that row by folding the HEAD records of the
+// following warps (in warp order, 32 at a time with a fixed lane tree) while they continue the same row
+template <class R>
+__global__ void __launch_bounds__(256) k_ragged_fix(RaggedParams p, int64_t nw) {
+  using B = typename R::B;
+  using A = typename R::A;
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (w >= nw) return;
+  const int64_t row = p.tail_row[w];
+  if (row < 0) return;
+  A acc = unpack<A>(p.tail_part[w]);
+  for (int64_t base = w + 1; base < nw; base += 32) {
+    const int64_t j = base + lane;
+    const int64_t hr = j < nw ? p.head_row[j] : -1;
+    const bool same = hr == row || hr == -2;
+    const unsigned m = __ballot_sync(FULL, same);
+    const unsigned run = ~m ? (m & ((1u << (__ffs(~m) - 1)) - 1u)) : m;  // contiguous prefix of matches
+    const bool take = (run >> lane) & 1u;
+    A v = take && hr == row ? unpack<A>(p.head_part[j]) : R::id();
+    acc = R::op(acc, R::warp(v));
+    if (run != 0xffffffffu) break;
+  }
+  if (lane == 0) {
+    if (p.has_init) acc = R::op(R::lift((B)p.init), acc);
+    ((B*)p.out)[row] = R::fin(acc);
   }
 }
 

@@ -58,6 +58,7 @@ def _load():
         "ipm_reduce": ([ci, ci, vp, i64, vp, vp, vp], ci),
         "ipm_reduce_async": ([ci, ci, vp, i64, vp, vp, vp, vp], ci),
         "ipm_reduce_segmented": ([ci, ci, vp, i64, i64, i64, vp, vp, vp, vp], ci),
+        "ipm_reduce_ragged": ([ci, ci, vp, vp, i64, vp, vp, vp, vp], ci),
         "ipm_reduce_partials": ([ci, ci, vp, i64, vp, ci, ctypes.POINTER(ci), vp], ci),
         "ipm_finalize_partials": ([ci, ci, vp, ci, vp, vp, vp], ci),
         "ipm_reduce_2d": ([ci, ci, vp, i64, i64, i64, vp, vp, vp], ci),
@@ -91,7 +92,7 @@ lib = _load()
 EXPORTED = ("ipm_status_str ipm_last_error_message ipm_op_legal ipm_dtype_size ipm_version ipm_set_allocator "
             "ipm_copyin ipm_create ipm_present ipm_update_device ipm_update_host ipm_copyout ipm_delete "
             "ipm_present_count ipm_workspace_bytes ipm_workspace_init ipm_reduce ipm_reduce_async "
-            "ipm_reduce_segmented ipm_reduce_partials ipm_finalize_partials ipm_reduce_2d ipm_reduce_2d_async ipm_fused_nvars ipm_reduce_fused ipm_reduce_fused_async ipm_reduce_host ipm_release_staging ipm_set_option ipm_profile_enable ipm_profile_read "
+            "ipm_reduce_segmented ipm_reduce_ragged ipm_reduce_partials ipm_finalize_partials ipm_reduce_2d ipm_reduce_2d_async ipm_fused_nvars ipm_reduce_fused ipm_reduce_fused_async ipm_reduce_host ipm_release_staging ipm_set_option ipm_profile_enable ipm_profile_read "
             "ipm_profile_disable ipm_flat_geometry ipm_comm_id_bytes "
             "ipm_comm_unique_id ipm_comm_init ipm_comm_destroy ipm_shard_range ipm_reduce_dist "
             "ipm_reduce_dist_async").split()
@@ -238,6 +239,24 @@ def reduce_segmented(op: str, t: torch.Tensor, rows: int | None = None, cols: in
     return out
 
 
+def reduce_ragged(op: str, values: torch.Tensor, offsets: torch.Tensor, init=None,
+                  out: torch.Tensor | None = None, ws: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Ragged (CSR) rows: out[r] = init ⊕ fold values[offsets[r]:offsets[r+1]] (offsets: int64 CUDA tensor of
+    rows+1 non-decreasing indices)."""
+    if not (values.is_cuda and offsets.is_cuda) or offsets.dtype != torch.int64 or not offsets.is_contiguous():
+        raise ValueError("values and offsets must be CUDA tensors, offsets contiguous int64")
+    ptr, _, dt = _flat_arg(values)
+    rows = offsets.numel() - 1
+    if out is None:
+        out = torch.empty(max(rows, 0), dtype=values.dtype, device=values.device)
+    ws = workspace(stream) if ws is None else ws
+    box = _scalar(dt, init)
+    _check(lib.ipm_reduce_ragged(op_code(op), dt, ptr, offsets.data_ptr(), rows,
+                                 None if box is None else box.ctypes.data, out.data_ptr(), ws.data_ptr(),
+                                 _stream(stream)), "ipm_reduce_ragged")
+    return out
+
+
 def reduce_partials(op: str, t: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     """The paper's first level alone: one accumulator-typed partial per thread block (8-byte slots, returned as
     a uint8 tensor view of int64 slots). See ipm.h for the slot format."""
@@ -355,7 +374,7 @@ def identity_value(op: str, dt: int):
     return out.cpu().numpy()[0]
 
 
-OPTIONS = {"flat_ctas_per_sm": 0, "seg_kernel": 1}
+OPTIONS = {"flat_ctas_per_sm": 0, "seg_kernel": 1, "deterministic": 2}
 SEG_KERNELS = {"auto": 0, "ldg": 1, "tma": 2}
 
 

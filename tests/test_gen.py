@@ -58,3 +58,17 @@ def test_iota_mod_const():
     # int32 iota wraps mod 2^32
     a = ipmgen.fill_host(ipmgen.Spec("int32", 3, "iota", param=2**31 - 2))
     assert list(a) == [2**31 - 2, 2**31 - 1, -2**31]
+
+
+def test_vectorised_draws_match_c():
+    idx = np.array([0, 1, 2, 1000, 2**40 + 7], dtype=np.uint64)
+    for seed in [0, 1, 0xD1B54A32D192ED03 ^ 5]:
+        assert list(ipmgen.draws(seed, idx)) == [ipmgen.h(seed, int(i)) for i in idx]
+
+
+def test_degrees():
+    d = ipmgen.degrees(200_000, seed=3)
+    assert d.min() >= 0 and 10 < d.mean() < 22 and d.max() > 1000      # heavy tail around mean 16
+    off = ipmgen.offsets_from_degrees(d, start=5)
+    assert off[0] == 5 and off[-1] == 5 + d.sum() and np.all(np.diff(off) == d)
+    assert np.array_equal(ipmgen.degrees(10, kind="const", mean=4), np.full(10, 4))

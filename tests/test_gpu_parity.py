@@ -342,3 +342,59 @@ def test_2d_view_api(ipm):
     sub = big[10:900, 33:650]
     assert ipm.reduce_2d("+", sub) == int(sub.sum())
     assert ipm.reduce_2d("max", sub) == int(sub.max())
+
+
+# --------------------------------------------------------------------------- ragged (CSR) rows
+
+def ragged_cases():
+    yield "tiny", np.array([0, 1, 1, 3], np.int64)
+    yield "all_empty", np.array([4] * 6, np.int64)
+    yield "one_row", np.array([0, 1000], np.int64)
+    yield "const", ipmgen.offsets_from_degrees(ipmgen.degrees(2000, kind="const", mean=33))
+    yield "uniform_off3", ipmgen.offsets_from_degrees(ipmgen.degrees(5000, kind="uniform", mean=20, seed=2), 3)
+    yield "powerlaw", ipmgen.offsets_from_degrees(ipmgen.degrees(20_000, seed=3))
+    d = np.zeros(300, np.int64); d[[0, 150, 299]] = [100_000, 1_000_000, 7]
+    yield "huge_rows", ipmgen.offsets_from_degrees(d)
+
+
+@pytest.mark.parametrize("op,dt", LEGAL)
+def test_ragged_parity(ipm, op, dt):
+    for k, (name, off) in enumerate(ragged_cases()):
+        n = int(off[-1]) + 5
+        spec = workload(op, dt, n, seed=k + 21)
+        x = device_input(spec, offset=k % 4)
+        offs = torch.from_numpy(off).cuda()
+        init = NPT[dt](2)
+        got = ipm.reduce_ragged(op, x, offs, init=init).cpu().numpy()
+        want_t, want_ld = oracle.reduce_ragged(op, ipmgen.fill_host(spec), off, init=init)
+        if dt.startswith("float") and op in ("+", "*"):
+            err = np.abs(got.astype(np.longdouble) - want_ld)
+            assert np.all((err <= TOL[dt] * np.abs(want_ld)) | (err == 0)), (op, dt, name)
+        else:
+            assert got.tobytes() == want_t.tobytes(), (op, dt, name)
+
+
+def test_ragged_big_powerlaw_deterministic(ipm):
+    off = ipmgen.offsets_from_degrees(ipmgen.degrees(1 << 20, seed=7))
+    spec = ipmgen.Spec("float32", int(off[-1]), "random", seed=7)
+    x = device_input(spec)
+    offs = torch.from_numpy(off).cuda()
+    a = ipm.reduce_ragged("+", x, offs).cpu().numpy()
+    b = ipm.reduce_ragged("+", x, offs).cpu().numpy()
+    assert a.tobytes() == b.tobytes()
+    _, want = oracle.reduce_ragged("+", ipmgen.fill_host(spec), off)
+    # dyadic data: row sums are exact in fp64 -> correctly rounded per row
+    assert np.array_equal(a, want.astype(np.float32))
+
+
+def test_nondeterministic_mode_parity(ipm):
+    ipm.set_option("deterministic", 0)
+    try:
+        for dt in ("float32", "float64"):
+            for n in [1, 1000, 4_000_037]:
+                spec = workload("+", dt, n, seed=n)
+                x = device_input(spec)
+                want_t, want_ld = oracle.reduce("+", ipmgen.fill_host(spec))
+                check("+", dt, ipm.reduce("+", x), want_t, want_ld)
+    finally:
+        ipm.set_option("deterministic", 1)

@@ -71,10 +71,12 @@ def run_case(name, dt, n, reps=30):
         ev1.record()
         ev1.synchronize()
         a = h.numpy().view(np.uint64)
-        s = init.astype(acc_np)            # the host loop over thread-block partials
-        for v in a:
-            s = s + np.array([v], dtype=np.uint64).view(np.float64)[0] if acc_np is np.float64 else \
-                np.uint32((int(s) + int(v & 0xFFFFFFFF)) & 0xFFFFFFFF)
+        # the host loop over thread-block partials, as compiled host code would run it (vectorised numpy)
+        if acc_np is np.float64:
+            s = float(init) + float(np.add.reduce(a.view(np.float64)))
+        else:
+            s = np.uint32((int(init) + int(np.add.reduce((a & 0xFFFFFFFF).astype(np.uint32), dtype=np.uint32)))
+                          & 0xFFFFFFFF)
         return (np.float32(s) if dt == "float32" else np.int32(np.uint32(s).view(np.int32))), ev0.elapsed_time(ev1)
 
     def multi_launch():

@@ -28,20 +28,22 @@ static float time_ms(std::function<void()> f, int reps) {
   return v[v.size() / 2];
 }
 
-template <class R, int BLOCK, int U, int HINT>
-void run_flat(const char* name, void* buf, size_t bytes, void* ws, int sms) {
+template <class R, int BLOCK, int U, int HINT, int SCHED = 0>
+void run_flat(const char* name, void* buf, size_t bytes, void* ws, int sms, int only_cps = 0) {
   int maxb = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&maxb, k_flat<R, BLOCK, U, HINT>, BLOCK, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&maxb, k_flat<R, BLOCK, U, HINT, SCHED>, BLOCK, 0));
   const int64_t n = bytes / sizeof(typename R::B);
   for (int cps = 1; cps <= maxb; cps *= 2) {
+    if (only_cps && cps != only_cps) continue;
     FlatParams p{};
     p.a = buf; p.n = n; p.row_stride = 0; p.init = 0; p.has_init = 0; p.mode = MODE_PARTIAL;
     p.out = (char*)ws + 4160; p.partials = (uint64_t*)((char*)ws + 8192); p.tickets = (unsigned*)ws;
+    p.counter = (unsigned long long*)((char*)ws + 4096 + 512);
     const int grid = sms * cps;
-    float ms = time_ms([&] { k_flat<R, BLOCK, U, HINT><<<grid, BLOCK>>>(p); }, 10);
+    float ms = time_ms([&] { k_flat<R, BLOCK, U, HINT, SCHED><<<grid, BLOCK>>>(p); }, 10);
     CK(cudaGetLastError());
-    printf("flat %-10s B=%4d U=%d H=%d cps=%d grid=%5d  %7.3f ms  %7.1f GB/s\n", name, BLOCK, U, HINT, cps, grid, ms,
-           bytes / ms / 1e6);
+    printf("flat %-10s B=%4d U=%d H=%d S=%d cps=%d grid=%5d  %7.3f ms  %7.1f GB/s\n", name, BLOCK, U, HINT, SCHED, cps,
+           grid, ms, bytes / ms / 1e6);
   }
 }
 
@@ -132,6 +134,33 @@ int main(int argc, char** argv) {
       run_seg_tma<Red<IPM_ADD, IPM_F32>, 8, 8, 2048>("f32+", buf, out, sms, rows, cols);
       run_seg_tma<Red<IPM_ADD, IPM_F32>, 4, 8, 4096>("f32+", buf, out, sms, rows, cols);
       run_seg_tma<Red<IPM_ADD, IPM_F32>, 2, 8, 8192>("f32+", buf, out, sms, rows, cols);
+    }
+  }
+  if (mode == "sched") {
+    for (size_t bytes : {(size_t)1 << 30, (size_t)4 << 30, (size_t)16 << 30}) {
+      printf("== sched %zu GiB\n", bytes >> 30);
+      run_flat<Red<IPM_ADD, IPM_F32>, 256, 4, 0, 0>("f32+", buf, bytes, ws, sms, 4);
+      run_flat<Red<IPM_ADD, IPM_F32>, 256, 4, 0, 1>("f32+", buf, bytes, ws, sms, 4);
+      run_flat<Red<IPM_ADD, IPM_F32>, 256, 4, 0, 2>("f32+", buf, bytes, ws, sms, 4);
+      run_flat<Red<IPM_ADD, IPM_F32>, 1024, 2, 0, 0>("f32+", buf, bytes, ws, sms, 1);
+      run_flat<Red<IPM_ADD, IPM_F32>, 1024, 2, 0, 1>("f32+", buf, bytes, ws, sms, 1);
+      run_flat<Red<IPM_ADD, IPM_F32>, 1024, 2, 0, 2>("f32+", buf, bytes, ws, sms, 1);
+      run_flat<Red<IPM_ADD, IPM_F32>, 512, 4, 0, 0>("f32+", buf, bytes, ws, sms, 0);
+      run_flat<Red<IPM_ADD, IPM_F32>, 512, 4, 0, 2>("f32+", buf, bytes, ws, sms, 0);
+      run_flat<Red<IPM_BXOR, IPM_I32>, 256, 4, 0, 0>("i32^", buf, bytes, ws, sms, 4);
+      run_flat<Red<IPM_BXOR, IPM_I32>, 256, 4, 0, 2>("i32^", buf, bytes, ws, sms, 4);
+      run_flat<Red<IPM_BXOR, IPM_I32>, 1024, 2, 0, 0>("i32^", buf, bytes, ws, sms, 1);
+      run_flat<Red<IPM_BXOR, IPM_I32>, 1024, 2, 0, 2>("i32^", buf, bytes, ws, sms, 1);
+      run_flat<Red<IPM_BXOR, IPM_I32>, 1024, 4, 0, 0>("i32^", buf, bytes, ws, sms, 1);
+      run_flat<Red<IPM_BXOR, IPM_I32>, 1024, 4, 0, 2>("i32^", buf, bytes, ws, sms, 1);
+      run_flat<Red<IPM_ADD, IPM_F64>, 256, 4, 0, 0>("f64+", buf, bytes, ws, sms, 4);
+      run_flat<Red<IPM_ADD, IPM_F64>, 256, 4, 0, 2>("f64+", buf, bytes, ws, sms, 4);
+      run_flat<Red<IPM_ADD, IPM_F64>, 1024, 2, 0, 0>("f64+", buf, bytes, ws, sms, 1);
+      run_flat<Red<IPM_ADD, IPM_F64>, 1024, 2, 0, 2>("f64+", buf, bytes, ws, sms, 1);
+      run_flat<Red<IPM_MAX, IPM_F64>, 1024, 2, 0, 0>("f64max", buf, bytes, ws, sms, 1);
+      run_flat<Red<IPM_MAX, IPM_F64>, 256, 4, 0, 0>("f64max", buf, bytes, ws, sms, 4);
+      run_flat<Red<IPM_MUL, IPM_I64>, 1024, 2, 0, 0>("i64*", buf, bytes, ws, sms, 1);
+      run_flat<Red<IPM_MUL, IPM_I64>, 1024, 2, 0, 2>("i64*", buf, bytes, ws, sms, 1);
     }
   }
   if (mode == "all" || mode == "big") {
