@@ -166,9 +166,13 @@ def suite(ipm, torch, ipmgen, peak):
     ws = ipm.workspace()
 
     def timed(fn, reps=20, flush=None):
-        for _ in range(3):
-            fn()
-        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        while True:  # clock spin-up: at least 3 calls and 0.1 s of back-to-back work before timing
+            for _ in range(3):
+                fn()
+            torch.cuda.synchronize()
+            if time.perf_counter() - t0 > 0.1:
+                break
         with ipm.KernelTimer(4 * reps) as kt:
             for _ in range(reps):
                 if flush is not None:
@@ -257,6 +261,21 @@ def suite(ipm, torch, ipmgen, peak):
     out["2d_float32_16384x16000_stride16384"] = {"kernel_ms_median": med, "GB/s": rows * cols * 4 / med / 1e6,
                                                  "frac": rows * cols * 4 / med / 1e6 / peak}
     del x, x2
+    # NEXT row 2: ragged (CSR) rows — power-law degree graph, 2^24 rows, mean degree 16 (BFS-style)
+    import numpy as np
+    off = ipmgen.offsets_from_degrees(ipmgen.degrees(1 << 24, seed=1, mean=16.0))
+    nnz = int(off[-1])
+    vals = torch.empty(nnz, dtype=torch.float32, device="cuda")
+    ipmgen.fill_tensor(ipmgen.Spec("float32", nnz, "random", seed=1), vals)
+    offs = torch.from_numpy(off).cuda()
+    o = torch.empty(1 << 24, dtype=torch.float32, device="cuda")
+    ms = timed(lambda: ipm.reduce_ragged("+", vals, offs, out=o, ws=ws))
+    med = statistics.median(ms)  # one record per call, covering both of its kernels
+    nbytes = nnz * 4 + off.size * 8 + (1 << 24) * 4
+    out["ragged_float32_powerlaw_2^24rows"] = {"nnz": nnz, "max_degree": int(np.diff(off).max()),
+                                               "ms_median": med, "GB/s": nbytes / med / 1e6,
+                                               "frac": nbytes / med / 1e6 / peak, "kernels_per_call": 2}
+    del vals, offs, o
     torch.cuda.empty_cache()
     return out
 
@@ -294,6 +313,13 @@ def run_ours(args, rank, world, local_rank):
             dist.barrier()
         torch.cuda.synchronize()
 
+    # clock spin-up (setup, untimed): back-to-back steps for >= 0.25 s so the timed steps run at steady clocks
+    t_spin = time.perf_counter()
+    spin = 0
+    while time.perf_counter() - t_spin < 0.25:
+        comm.reduce_async("+", x, init=init, out=out, ws=ws)
+        torch.cuda.synchronize()
+        spin += 1
     for _ in range(args.warmup):
         comm.reduce_async("+", x, init=init, out=out, ws=ws)
     barrier()
@@ -398,7 +424,7 @@ def run_ours(args, rank, world, local_rank):
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": 2 * args.steps,
             "gpu_launches_note": "per step: 1 k_flat + 1 k_finalize (plus NCCL's own AllGather kernel)",
-            "clocks": clk.summary(), "result_rank0": result,
+            "clocks": clk.summary(), "result_rank0": result, "spinup_steps": spin,
         }
         if st is not None:
             line["suite"] = st

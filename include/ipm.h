@@ -215,10 +215,11 @@ ipm_status ipm_profile_disable(void);
  *   IPM_OPT_FLAT_CTAS_PER_SM  CTAs per SM of the flat kernel's persistent grid, 1..8 (-1 = default 4)
  *   IPM_OPT_SEG_KERNEL        segmented rows: 0 auto (direct 256-bit loads), 1 direct loads, 2 TMA bulk copies
  *                             into a per-warp shared-memory ring (rows of >= 64 bytes)
- *   IPM_OPT_DETERMINISTIC     1 (default): float + and * of the flat clause use a static tile schedule, so
- *                             repeated runs give identical bits; 0: every op takes tiles dynamically (faster
- *                             on some sizes; float results may then differ in the last bits between runs).
- *                             Exact operators always use the dynamic schedule.
+ *   IPM_OPT_DETERMINISTIC     1 (default): the flat clause uses the guided schedule — ~90% of the tiles
+ *                             dealt statically, the rest in fixed chunks claimed dynamically, one partial per
+ *                             element range, folded in a fixed order — so repeated runs give identical bits
+ *                             for every op; 0: purely dynamic tiles (float + and * may then differ in the last
+ *                             bits between runs).
  * IPM_E_ARG for an unknown key or an out-of-range value. */
 typedef enum { IPM_OPT_FLAT_CTAS_PER_SM = 0, IPM_OPT_SEG_KERNEL = 1, IPM_OPT_DETERMINISTIC = 2 } ipm_option;
 ipm_status ipm_set_option(ipm_option key, int64_t value);

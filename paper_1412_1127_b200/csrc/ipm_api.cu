@@ -152,16 +152,18 @@ static void prof_free() {
 template <int OP, int DT>
 struct Launch {
   using R = Red<OP, DT>;
-  // exact operators (every result bit independent of the grouping) take tiles dynamically from an atomic
-  // counter, which absorbs per-SM bandwidth differences (tools/sweep_flat.cu: +2% at 16 GiB, +11% at 1 GiB);
-  // float + and * keep the static grid-stride schedule so that their rounding, hence their bits, are the
-  // same on every run (IPM_OPT_DETERMINISTIC, default 1).
-  static constexpr bool kExact = !((DT == IPM_F32 || DT == IPM_F64) && (OP == IPM_ADD || OP == IPM_MUL));
+  // the flat clause uses the guided schedule (k_flat_guided: ~90% of the tiles static, the rest in chunks
+  // claimed dynamically, one partial slot per element range) — load-balanced and bit-reproducible for every
+  // operator. IPM_OPT_DETERMINISTIC = 0 selects the purely dynamic tile schedule instead (float + and * may
+  // then differ in the last bits between runs). Multi-row launches (grid.y > 1) and the per-block partials
+  // mode keep the static grid-stride schedule.
   static void flat(const FlatParams& p, dim3 grid, cudaStream_t st) {
-    if (p.counter && grid.y == 1 && (kExact || !g_opt_deterministic))
-      k_flat<R, FLAT_BLOCK, FLAT_U, 0, 2><<<grid, FLAT_BLOCK, 0, st>>>(p);
-    else
+    if (p.counter && grid.y == 1 && grid.x > 1) {
+      if (g_opt_deterministic) k_flat_guided<R, FLAT_BLOCK, FLAT_U><<<grid, FLAT_BLOCK, 0, st>>>(p);
+      else k_flat<R, FLAT_BLOCK, FLAT_U, 0, 2><<<grid, FLAT_BLOCK, 0, st>>>(p);
+    } else {
       k_flat<R, FLAT_BLOCK, FLAT_U, 0, 0><<<grid, FLAT_BLOCK, 0, st>>>(p);
+    }
   }
   static void seg_warp(const SegParams& p, int grid, cudaStream_t st) {
     k_seg_warp<R, SEG_WARPS, SEG_U><<<grid, SEG_WARPS * 32, 0, st>>>(p);
@@ -255,9 +257,11 @@ ipm_status launch_flat(ipm_op op, ipm_dtype dt, const void* dev, int64_t n, uint
   p.partials = (uint64_t*)((char*)ws + WS_PARTIALS);
   p.tickets = (unsigned*)((char*)ws + WS_TICKETS);
   p.counter = (unsigned long long*)((char*)ws + WS_COUNTER);
+  const int64_t grid = flat_grid(dt, n);
+  p.max_chunks = std::max<int64_t>(1, WS_MAX_PARTIALS - grid - 1);
   {
     ProfScope ps(st, 0);
-    t->flat(p, dim3((unsigned)flat_grid(dt, n), 1, 1), st);
+    t->flat(p, dim3((unsigned)grid, 1, 1), st);
   }
   CK(cudaGetLastError());
   return IPM_OK;
@@ -560,6 +564,7 @@ ipm_status ipm_reduce_segmented(ipm_op op, ipm_dtype dt, const void* dev, int64_
     p.partials = ws ? (uint64_t*)((char*)ws + WS_PARTIALS) : nullptr;
     p.tickets = ws ? (unsigned*)((char*)ws + WS_TICKETS) : nullptr;
     p.counter = nullptr;
+    p.max_chunks = 0;
     {
       ProfScope ps(st, 1);
       t->flat(p, dim3((unsigned)S, (unsigned)rows, 1), st);
@@ -619,6 +624,7 @@ ipm_status ipm_reduce_partials(ipm_op op, ipm_dtype dt, const void* dev, int64_t
   p.partials = nullptr;
   p.tickets = nullptr;
   p.counter = nullptr;
+  p.max_chunks = 0;
   cudaStream_t st = (cudaStream_t)stream;
   {
     ProfScope ps(st, 0);
@@ -726,6 +732,7 @@ ipm_status ipm_reduce_2d_async(ipm_op op, ipm_dtype dt, const void* dev, int64_t
   q.f.partials = (uint64_t*)((char*)ws + WS_PARTIALS);
   q.f.tickets = (unsigned*)((char*)ws + WS_TICKETS);
   q.f.counter = nullptr;
+  q.f.max_chunks = 0;
   q.rows = rows;
   q.cols = cols;
   q.row_stride = row_stride;

@@ -44,13 +44,15 @@ struct Vec<uint64_t> {
 // HINT selects the cache policy (tools/sweep_flat.cu measures them; the product uses 0):
 //   0 ld.global.nc.L1::no_allocate.L2::evict_first.L2::256B   1 ld.global.nc.L1::no_allocate
 //   2 ld.global (plain)                                         3 ld.global.nc.L1::no_allocate.L2::256B
+// `asm volatile`: a plain asm statement is a pure function to the compiler, which may then hoist or speculate
+// the load past the branch that guards it (observed: a guarded tile load executed for an out-of-range tile).
 #define IPM_LDV8(Q)                                                                                   \
-  asm(Q ".v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"                                                   \
+  asm volatile(Q ".v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"                                                   \
       : "=r"(v.w[0]), "=r"(v.w[1]), "=r"(v.w[2]), "=r"(v.w[3]), "=r"(v.w[4]), "=r"(v.w[5]), "=r"(v.w[6]), \
         "=r"(v.w[7])                                                                                  \
       : "l"(p))
 #define IPM_LDV4(Q) \
-  asm(Q ".v4.b64 {%0,%1,%2,%3}, [%4];" : "=l"(v.w[0]), "=l"(v.w[1]), "=l"(v.w[2]), "=l"(v.w[3]) : "l"(p))
+  asm volatile(Q ".v4.b64 {%0,%1,%2,%3}, [%4];" : "=l"(v.w[0]), "=l"(v.w[1]), "=l"(v.w[2]), "=l"(v.w[3]) : "l"(p))
 template <int HINT = 0>
 __device__ __forceinline__ V8 ldv(const V8* p) {
   V8 v;
@@ -87,7 +89,8 @@ struct FlatParams {
   void* out;
   uint64_t* partials;     // gridDim.x * gridDim.y slots (unused when gridDim.x == 1)
   unsigned* tickets;      // gridDim.y tickets (unused when gridDim.x == 1); left at zero
-  unsigned long long* counter;  // SCHED 2 only: dynamic tile counter, left at zero
+  unsigned long long* counter;  // dynamic schedules: tile / chunk counter, left at zero
+  int64_t max_chunks;     // k_flat_guided: partial slots available for dynamic chunks
 };
 enum { MODE_RESULT = 0, MODE_PARTIAL = 1, MODE_ACCUM_FIRST = 2, MODE_ACCUM = 3, MODE_CTA_PARTIALS = 4 };
 
@@ -168,7 +171,7 @@ __device__ __forceinline__ void grid_finish(const FlatParams& p, int64_t row, ty
 // range per CTA, 2 dynamic (an atomic tile counter; absorbs per-SM bandwidth differences). tools/sweep_flat.cu
 // measures them.
 template <class R, int BLOCK, int U, int HINT = 0, int SCHED = 0>
-__global__ void __launch_bounds__(BLOCK) k_flat(FlatParams p) {
+__global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_flat(FlatParams p) {
   using B = typename R::B;
   using A = typename R::A;
   using VT = typename Vec<B>::T;
@@ -240,6 +243,121 @@ __global__ void __launch_bounds__(BLOCK) k_flat(FlatParams p) {
   // a4 + a5
   A cta = block_reduce<R, BLOCK>(acc[0], sm);
   grid_finish<R, BLOCK>(p, row, cta, sm);
+}
+
+// ------------------------------------------------------------------------------------------ flat, guided
+// Deterministic AND load-balanced schedule ("guided self-scheduling"): about 90% of the tiles are dealt
+// statically, grid-stride (CTA b folds tiles b, b+G, b+2G, ... into partial slot b); the rest is cut into K
+// fixed chunks of ct contiguous tiles that CTAs claim from an atomic counter as they finish (chunk c ->
+// partial slot G + c), and one last "chunk" K holds the ragged remainder (vectors past the last whole tile,
+// head and tail scalars). Every slot's value depends only on its element range and the fixed thread mapping —
+// not on which CTA computed it — and the last CTA folds the G + K + 1 slots in slot order, so the result is
+// bit-identical run to run while fast SMs absorb the slow ones' share of the tail.
+template <class R, int BLOCK, int U>
+__global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_flat_guided(FlatParams p) {
+  using B = typename R::B;
+  using A = typename R::A;
+  using VT = typename Vec<B>::T;
+  constexpr int VW = Vec<B>::W;
+  constexpr int64_t TILE = (int64_t)BLOCK * U;
+  __shared__ A sm[BLOCK / 32];
+  __shared__ long long s_c;
+  __shared__ int s_last;
+  const B* a = (const B*)p.a;
+  const int64_t n = p.n;
+  const uintptr_t addr = (uintptr_t)a;
+  int64_t head = (int64_t)(((32u - (addr & 31u)) & 31u) / sizeof(B));
+  if (head > n) head = n;
+  const int64_t nv = (n - head) / VW;
+  const int64_t tail0 = head + nv * VW;
+  const VT* vp = (const VT*)(a + head);
+  const int64_t ntiles = nv / TILE;
+  const int64_t G = gridDim.x;
+  const int64_t srounds = (ntiles - ntiles / 10) / G;   // static rounds per CTA (~90% of the tiles)
+  const int64_t dyn0 = srounds * G;
+  const int64_t rem = ntiles - dyn0;
+  const int64_t max_chunks = p.max_chunks > 0 ? p.max_chunks : 1;
+  const int64_t ct = rem > 0 ? (rem + max_chunks - 1) / max_chunks : 1;
+  const int64_t K = (rem + ct - 1) / ct;                 // dynamic chunks 0..K-1; chunk K = the remainder
+  uint64_t* slots = p.partials;
+
+  A acc[VW];
+  auto reset = [&]() {
+#pragma unroll
+    for (int k = 0; k < VW; ++k) acc[k] = R::id();
+  };
+  auto tile = [&](int64_t t) {
+#ifdef IPM_GUIDED_DEBUG
+    if (t < 0 || t >= ntiles) {
+      printf("OOB tile %lld ntiles %lld block %d thread %d G %lld srounds %lld K %lld ct %lld dyn0 %lld\n",
+             (long long)t, (long long)ntiles, blockIdx.x, threadIdx.x, (long long)G, (long long)srounds,
+             (long long)K, (long long)ct, (long long)dyn0);
+      __trap();
+    }
+#endif
+    const VT* base = vp + t * TILE + threadIdx.x;
+    VT v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = ldv(base + u * BLOCK);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int k = 0; k < VW; ++k) acc[k] = R::op(acc[k], R::lift(v[u].w[k]));
+  };
+  auto publish = [&](int64_t slot) {  // fixed tree: VW lanes -> warp -> CTA; one slot per element range
+#pragma unroll
+    for (int s2 = VW / 2; s2 > 0; s2 >>= 1)
+#pragma unroll
+      for (int k = 0; k < s2; ++k) acc[k] = R::op(acc[k], acc[k + s2]);
+    const A t = block_reduce<R, BLOCK>(acc[0], sm);
+    if (threadIdx.x == 0) __stcg(slots + slot, pack(t));
+    __syncthreads();  // sm reuse
+  };
+
+  // static part
+  reset();
+  for (int64_t k = 0; k < srounds; ++k) tile(blockIdx.x + k * G);
+  if (threadIdx.x == 0) s_c = (long long)atomicAdd(p.counter, 1ull);  // claim the first dynamic chunk
+  publish(blockIdx.x);
+  long long c = s_c;
+  // dynamic part: chunks claimed until the counter passes the remainder chunk
+  while (c <= K) {
+    __syncthreads();  // everyone has read s_c
+    if (threadIdx.x == 0) s_c = (long long)atomicAdd(p.counter, 1ull);  // claim the next chunk early
+    reset();
+    if (c < K) {
+      const int64_t e1 = dyn0 + (int64_t)(c + 1) * ct;
+      const int64_t t1 = e1 < ntiles ? e1 : ntiles;
+      for (int64_t t = dyn0 + (int64_t)c * ct; t < t1; ++t) tile(t);
+    } else {
+      for (int64_t i = ntiles * TILE + threadIdx.x; i < nv; i += BLOCK) {
+        const VT v = ldv(vp + i);
+#pragma unroll
+        for (int k = 0; k < VW; ++k) acc[k] = R::op(acc[k], R::lift(v.w[k]));
+      }
+      if (threadIdx.x < head) acc[0] = R::op(acc[0], R::lift(lds(a + threadIdx.x)));
+      if (threadIdx.x < n - tail0) acc[VW - 1] = R::op(acc[VW - 1], R::lift(lds(a + tail0 + threadIdx.x)));
+    }
+    publish(G + c);
+    c = s_c;
+  }
+  // the CTA that takes the last ticket folds all slots (fixed thread -> slot mapping and tree)
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(p.tickets, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int64_t nslots = G + K + 1;
+  A v = R::id();
+  for (int64_t i = threadIdx.x; i < nslots; i += BLOCK) v = R::op(v, unpack<A>(__ldcg(slots + i)));
+  const A total = block_reduce<R, BLOCK>(v, sm);
+  if (threadIdx.x == 0) {
+    store_out<R>(p, 0, total);
+    *p.tickets = 0u;
+    *p.counter = 0ull;
+  }
 }
 
 // ------------------------------------------------------------------------------------------ 2-D collapse

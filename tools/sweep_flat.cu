@@ -78,6 +78,20 @@ void run_seg_tma(const char* name, void* buf, void* out, int sms, int64_t rows, 
   }
 }
 
+template <class R>
+void run_guided(const char* name, void* buf, size_t bytes, void* ws, int sms) {
+  const int64_t n = bytes / sizeof(typename R::B);
+  FlatParams p{};
+  p.a = buf; p.n = n; p.row_stride = 0; p.init = 0; p.has_init = 0; p.mode = MODE_PARTIAL;
+  p.out = (char*)ws + 4160; p.partials = (uint64_t*)((char*)ws + 8192); p.tickets = (unsigned*)ws;
+  p.counter = (unsigned long long*)((char*)ws + 4096 + 512);
+  const int grid = sms * 4;
+  p.max_chunks = 16384 - grid - 1;
+  float ms = time_ms([&] { k_flat_guided<R, 256, 4><<<grid, 256>>>(p); }, 20);
+  CK(cudaGetLastError());
+  printf("guided %-8s B= 256 U=4 cps=4 grid=%5d  %7.3f ms  %7.1f GB/s\n", name, grid, ms, bytes / ms / 1e6);
+}
+
 int main(int argc, char** argv) {
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
@@ -161,6 +175,28 @@ int main(int argc, char** argv) {
       run_flat<Red<IPM_MAX, IPM_F64>, 256, 4, 0, 0>("f64max", buf, bytes, ws, sms, 4);
       run_flat<Red<IPM_MUL, IPM_I64>, 1024, 2, 0, 0>("i64*", buf, bytes, ws, sms, 1);
       run_flat<Red<IPM_MUL, IPM_I64>, 1024, 2, 0, 2>("i64*", buf, bytes, ws, sms, 1);
+    }
+  }
+  if (mode == "guided") {
+    // spin the clocks up first
+    for (int i = 0; i < 30; ++i) k_flat<Red<IPM_ADD, IPM_F32>, 256, 4, 0, 0><<<sms * 4, 256>>>(FlatParams{buf, (int64_t)(big / 4), 0, 0, 0, MODE_PARTIAL, (char*)ws + 4160, (uint64_t*)((char*)ws + 8192), (unsigned*)ws, nullptr, 0});
+    CK(cudaDeviceSynchronize());
+    for (size_t bytes : {(size_t)1 << 30, (size_t)4 << 30, (size_t)16 << 30}) {
+      printf("== guided %zu GiB\n", bytes >> 30);
+      for (int rep = 0; rep < 2; ++rep) {
+        run_flat<Red<IPM_ADD, IPM_F32>, 256, 4, 0, 0>("f32+", buf, bytes, ws, sms, 4);
+        run_flat<Red<IPM_ADD, IPM_F32>, 256, 4, 0, 2>("f32+", buf, bytes, ws, sms, 4);
+        run_guided<Red<IPM_ADD, IPM_F32>>("f32+", buf, bytes, ws, sms);
+        run_flat<Red<IPM_ADD, IPM_F64>, 256, 4, 0, 0>("f64+", buf, bytes, ws, sms, 4);
+        run_flat<Red<IPM_ADD, IPM_F64>, 256, 4, 0, 2>("f64+", buf, bytes, ws, sms, 4);
+        run_guided<Red<IPM_ADD, IPM_F64>>("f64+", buf, bytes, ws, sms);
+        run_flat<Red<IPM_BXOR, IPM_I32>, 256, 4, 0, 0>("i32^", buf, bytes, ws, sms, 4);
+        run_flat<Red<IPM_BXOR, IPM_I32>, 256, 4, 0, 2>("i32^", buf, bytes, ws, sms, 4);
+        run_guided<Red<IPM_BXOR, IPM_I32>>("i32^", buf, bytes, ws, sms);
+        run_guided<Red<IPM_MAX, IPM_F32>>("f32max", buf, bytes, ws, sms);
+        run_guided<Red<IPM_MUL, IPM_I64>>("i64*", buf, bytes, ws, sms);
+        run_guided<Red<IPM_MAX, IPM_F64>>("f64max", buf, bytes, ws, sms);
+      }
     }
   }
   if (mode == "all" || mode == "big") {
