@@ -219,9 +219,15 @@ ipm_status ipm_profile_disable(void);
  *                             dealt statically, the rest in fixed chunks claimed dynamically, one partial per
  *                             element range, folded in a fixed order — so repeated runs give identical bits
  *                             for every op; 0: purely dynamic tiles (float + and * may then differ in the last
- *                             bits between runs).
+ *                             bits between runs); 2: static grid-stride tiles (deterministic, no balancing).
  * IPM_E_ARG for an unknown key or an out-of-range value. */
-typedef enum { IPM_OPT_FLAT_CTAS_PER_SM = 0, IPM_OPT_SEG_KERNEL = 1, IPM_OPT_DETERMINISTIC = 2 } ipm_option;
+typedef enum {
+  IPM_OPT_FLAT_CTAS_PER_SM = 0,
+  IPM_OPT_SEG_KERNEL = 1,
+  IPM_OPT_DETERMINISTIC = 2,
+  IPM_OPT_DIST_MODE = 3,        /* 0 (default): fused peer-memory exchange when every peer is mapped; 1: NCCL */
+  IPM_OPT_DIST_TIMEOUT_MS = 4   /* fused exchange: give up waiting for a peer after this long (default 30000) */
+} ipm_option;
 ipm_status ipm_set_option(ipm_option key, int64_t value);
 
 /* Launch geometry the library uses for a flat reduce of n elements (for tests and the roofline report). */
@@ -245,6 +251,13 @@ ipm_status ipm_shard_range(int64_t n, int rank, int world, int64_t* lo, int64_t*
  * the global result (out). Blocks until *inout is written. */
 ipm_status ipm_reduce_dist(ipm_comm* comm, ipm_op op, ipm_dtype dt, const void* dev_shard, int64_t n_shard,
                            void* inout, void* workspace, void* stream);
+/* 1 if ipm_reduce_dist on this communicator takes the fused path: every peer's symmetric slot buffer is mapped
+ * (CUDA IPC over NVLink) and IPM_OPT_DIST_MODE is 0 — the reduction kernel then exchanges the rank partials
+ * itself (one kernel per rank per call). 0: ncclAllGather + a one-warp fold kernel. */
+int ipm_comm_uses_peer_memory(const ipm_comm* comm);
+/* Fused path only: *err = 1 if a call since the last check gave up waiting for a peer (IPM_OPT_DIST_TIMEOUT_MS);
+ * the flag is cleared. ipm_reduce_dist checks it itself and returns IPM_E_NCCL. */
+ipm_status ipm_comm_error(ipm_comm* comm, int* err);
 /* Asynchronous form: result written to dev_result (device, one element) in stream order. */
 ipm_status ipm_reduce_dist_async(ipm_comm* comm, ipm_op op, ipm_dtype dt, const void* dev_shard,
                                  int64_t n_shard, const void* init, void* dev_result, void* workspace,

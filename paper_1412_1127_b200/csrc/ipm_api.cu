@@ -54,7 +54,9 @@ constexpr int FLAT_U = 4;  // 4 x 32 B in flight per thread
 // run-time options (ipm_set_option); defaults chosen by tools/sweep_flat.cu measurements
 static int g_opt_flat_cps = -1;  // CTAs per SM for k_flat (-1: IPM_CTAS_PER_SM env or 4)
 static int g_opt_seg_kernel = 0; // 0 auto, 1 k_seg_warp (LDG), 2 k_seg_tma (bulk copies)
-static int g_opt_deterministic = 1;  // 1: float + and * keep a static schedule (bit-reproducible)
+static int g_opt_deterministic = 1;  // 1: guided deterministic schedule for the flat kernel
+static int g_opt_dist_mode = 0;      // 0: fused peer-memory exchange when mapped, 1: NCCL AllGather
+static long long g_opt_dist_timeout_ms = 30000;
 static int flat_ctas_per_sm() {
   if (g_opt_flat_cps > 0) return g_opt_flat_cps;
   static int v = std::max(1, std::min(8, env_int("IPM_CTAS_PER_SM", 4)));
@@ -138,6 +140,9 @@ static void prof_free() {
   g_prof = Prof();
 }
 
+int dist_mode_option() { return g_opt_dist_mode; }
+long long dist_timeout_ns() { return g_opt_dist_timeout_ms * 1000000ll; }
+
 // ------------------------------------------------------------------------------------------ dispatch
 #define IPM_LEGAL(X)                                                                                       \
   X(IPM_ADD, IPM_I32) X(IPM_MUL, IPM_I32) X(IPM_MAX, IPM_I32) X(IPM_MIN, IPM_I32) X(IPM_BAND, IPM_I32)     \
@@ -158,7 +163,7 @@ struct Launch {
   // then differ in the last bits between runs). Multi-row launches (grid.y > 1) and the per-block partials
   // mode keep the static grid-stride schedule.
   static void flat(const FlatParams& p, dim3 grid, cudaStream_t st) {
-    if (p.counter && grid.y == 1 && grid.x > 1) {
+    if (p.counter && grid.y == 1 && grid.x > 1 && g_opt_deterministic != 2) {
       if (g_opt_deterministic) k_flat_guided<R, FLAT_BLOCK, FLAT_U><<<grid, FLAT_BLOCK, 0, st>>>(p);
       else k_flat<R, FLAT_BLOCK, FLAT_U, 0, 2><<<grid, FLAT_BLOCK, 0, st>>>(p);
     } else {
@@ -244,7 +249,7 @@ static ipm_status check_array(ipm_dtype dt, const void* dev, int64_t n) {
 }
 
 ipm_status launch_flat(ipm_op op, ipm_dtype dt, const void* dev, int64_t n, uint64_t init, int has_init, int mode,
-                       void* out, void* ws, cudaStream_t st) {
+                       void* out, void* ws, cudaStream_t st, const DistArgs* dist) {
   const Table* t = table(op, dt);
   FlatParams p;
   p.a = dev;
@@ -259,6 +264,10 @@ ipm_status launch_flat(ipm_op op, ipm_dtype dt, const void* dev, int64_t n, uint
   p.counter = (unsigned long long*)((char*)ws + WS_COUNTER);
   const int64_t grid = flat_grid(dt, n);
   p.max_chunks = std::max<int64_t>(1, WS_MAX_PARTIALS - grid - 1);
+  p.peers = dist ? dist->peers : nullptr;
+  p.rank = dist ? dist->rank : 0;
+  p.world = dist ? dist->world : 1;
+  p.timeout_ns = dist ? dist->timeout_ns : 0;
   {
     ProfScope ps(st, 0);
     t->flat(p, dim3((unsigned)grid, 1, 1), st);
@@ -430,8 +439,16 @@ ipm_status ipm_set_option(ipm_option key, int64_t value) {
       g_opt_seg_kernel = (int)value;
       return IPM_OK;
     case IPM_OPT_DETERMINISTIC:
-      if (value < 0 || value > 1) break;
+      if (value < 0 || value > 2) break;
       g_opt_deterministic = (int)value;
+      return IPM_OK;
+    case IPM_OPT_DIST_MODE:
+      if (value < 0 || value > 1) break;
+      g_opt_dist_mode = (int)value;
+      return IPM_OK;
+    case IPM_OPT_DIST_TIMEOUT_MS:
+      if (value < 1) break;
+      g_opt_dist_timeout_ms = value;
       return IPM_OK;
   }
   set_error("unknown option or value out of range");
@@ -565,6 +582,10 @@ ipm_status ipm_reduce_segmented(ipm_op op, ipm_dtype dt, const void* dev, int64_
     p.tickets = ws ? (unsigned*)((char*)ws + WS_TICKETS) : nullptr;
     p.counter = nullptr;
     p.max_chunks = 0;
+    p.peers = nullptr;
+    p.rank = 0;
+    p.world = 1;
+    p.timeout_ns = 0;
     {
       ProfScope ps(st, 1);
       t->flat(p, dim3((unsigned)S, (unsigned)rows, 1), st);
@@ -625,6 +646,10 @@ ipm_status ipm_reduce_partials(ipm_op op, ipm_dtype dt, const void* dev, int64_t
   p.tickets = nullptr;
   p.counter = nullptr;
   p.max_chunks = 0;
+  p.peers = nullptr;
+  p.rank = 0;
+  p.world = 1;
+  p.timeout_ns = 0;
   cudaStream_t st = (cudaStream_t)stream;
   {
     ProfScope ps(st, 0);
@@ -733,6 +758,10 @@ ipm_status ipm_reduce_2d_async(ipm_op op, ipm_dtype dt, const void* dev, int64_t
   q.f.tickets = (unsigned*)((char*)ws + WS_TICKETS);
   q.f.counter = nullptr;
   q.f.max_chunks = 0;
+  q.f.peers = nullptr;
+  q.f.rank = 0;
+  q.f.world = 1;
+  q.f.timeout_ns = 0;
   q.rows = rows;
   q.cols = cols;
   q.row_stride = row_stride;

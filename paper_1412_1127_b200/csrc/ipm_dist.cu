@@ -1,12 +1,17 @@
-// ipm_dist.cu — the multi-GPU clause (a9): contiguous shards, one NCCL collective, rank-ordered fold.
+// ipm_dist.cu — the multi-GPU clause (a9): contiguous shards, one exchange of accumulator partials, a fold in
+// rank order.
 //
-// Each rank reduces its shard with the single-GPU kernel into an ACCUMULATOR-typed partial (float32 `+`
-// stays float64, so rounding happens once, globally), one ncclAllGather moves the P partials (8 bytes
-// each) over NVLink/NVSwitch, and a one-warp kernel folds them in rank order, merges the variable's
-// original value and rounds. AllGather + an ordered fold (rather than ncclAllReduce) is used for every op:
-// NCCL has no & | ^ (nccl.h ncclRedOp_t: Sum, Prod, Max, Min, Avg), and an ordered fold gives every rank
-// the same bits whatever NCCL's internal reduction order (ring / tree / NVLS). The message is 8 bytes per
-// rank, so the collective is latency-bound either way.
+// Each rank reduces its shard into an ACCUMULATOR-typed partial (float32 `+` stays float64, so rounding
+// happens once, globally). Two exchanges, same result bits:
+//   fused (default when every peer's buffer is mapped): the reduction kernel itself, in the CTA that finishes
+//     the shard, stores the partial into every peer's symmetric slot buffer over NVLink (CUDA IPC peer
+//     mappings), waits for all ranks' slots, folds them in rank order and writes the result — ONE kernel per
+//     rank, no collective launch, no second kernel (ipm_kernels.cuh dist_exchange);
+//   NCCL: the kernel writes the partial, one ncclAllGather moves the P partials (8 bytes each), a one-warp
+//     kernel folds them in rank order. AllGather + an ordered fold (rather than ncclAllReduce) because NCCL has
+//     no & | ^ (nccl.h ncclRedOp_t: Sum, Prod, Max, Min, Avg) and so that every rank gets the same bits
+//     whatever NCCL's internal reduction order.
+// The message is 8 bytes per rank: both are latency-bound; the fused path removes two launches per call.
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -15,10 +20,15 @@
 
 #include "ipm.h"
 #include "ipm_internal.h"
+#include "ipm_kernels.cuh"
 
 struct ipm_comm {
   ncclComm_t nccl;
   int rank, world, device;
+  int p2p;                      // every peer's symmetric buffer is mapped into this process
+  uint64_t* sym;                // own symmetric slot buffer (cudaMalloc, IPC-exported)
+  uint64_t** peers_dev;         // device array of world pointers (own buffer at [rank])
+  void* opened[64];             // peer mappings to close
 };
 
 using namespace ipm;
@@ -26,6 +36,61 @@ using namespace ipm;
 static ipm_status nccl_fail(ncclResult_t r, const char* where) {
   set_error(std::string(where) + ": " + ncclGetErrorString(r));
   return IPM_E_NCCL;
+}
+
+// symmetric slot buffers: allocate and IPC-export one per rank, exchange the handles with one ncclAllGather,
+// map every peer's buffer; all ranks then agree (ncclAllReduce min) on whether the fused path is usable.
+constexpr size_t SYM_BYTES = 8 * 1024;  // >= SYM_WORDS * 8
+static ipm_status setup_peer_memory(ipm_comm* m) {
+  cudaError_t e;
+  if ((e = cudaMalloc(&m->sym, SYM_BYTES)) != cudaSuccess) return cuda_fail(e, "cudaMalloc(sym)");
+  if ((e = cudaMemset(m->sym, 0, SYM_BYTES)) != cudaSuccess) return cuda_fail(e, "cudaMemset(sym)");
+  uint64_t* host_ptrs[64] = {nullptr};
+  host_ptrs[m->rank] = m->sym;
+  int ok = 1;
+  if (m->world > 1) {
+    cudaIpcMemHandle_t mine;
+    if (cudaIpcGetMemHandle(&mine, m->sym) != cudaSuccess) ok = 0;
+    char* dbuf = nullptr;
+    const size_t hb = sizeof(cudaIpcMemHandle_t);
+    if ((e = cudaMalloc(&dbuf, hb * m->world + sizeof(int))) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+    cudaMemcpy(dbuf + hb * m->rank, &mine, hb, cudaMemcpyHostToDevice);
+    ncclResult_t r = ncclAllGather(dbuf + hb * m->rank, dbuf, hb, ncclUint8, m->nccl, 0);
+    if (r != ncclSuccess) {
+      cudaFree(dbuf);
+      return nccl_fail(r, "ncclAllGather(ipc handles)");
+    }
+    std::string all(hb * m->world, '\0');
+    if ((e = cudaMemcpy(&all[0], dbuf, hb * m->world, cudaMemcpyDeviceToHost)) != cudaSuccess) {
+      cudaFree(dbuf);
+      return cuda_fail(e, "cudaMemcpy(handles)");
+    }
+    for (int q = 0; q < m->world && ok; ++q) {
+      if (q == m->rank) continue;
+      cudaIpcMemHandle_t h;
+      memcpy(&h, &all[hb * q], hb);
+      void* ptr = nullptr;
+      if (cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        ok = 0;
+        break;
+      }
+      m->opened[q] = ptr;
+      host_ptrs[q] = (uint64_t*)ptr;
+    }
+    // every rank must take the same path
+    int* dok = (int*)(dbuf + hb * m->world);
+    cudaMemcpy(dok, &ok, sizeof(int), cudaMemcpyHostToDevice);
+    r = ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, m->nccl, 0);
+    if (r == ncclSuccess) cudaMemcpy(&ok, dok, sizeof(int), cudaMemcpyDeviceToHost);
+    else ok = 0;
+    cudaFree(dbuf);
+  }
+  if ((e = cudaMalloc(&m->peers_dev, sizeof(uint64_t*) * m->world)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+  if ((e = cudaMemcpy(m->peers_dev, host_ptrs, sizeof(uint64_t*) * m->world, cudaMemcpyHostToDevice)) != cudaSuccess)
+    return cuda_fail(e, "cudaMemcpy(peers)");
+  m->p2p = ok;
+  return IPM_OK;
 }
 
 extern "C" {
@@ -60,12 +125,27 @@ ipm_status ipm_comm_init(ipm_comm** comm, int rank, int world, const void* id, i
   ncclComm_t c;
   ncclResult_t r = ncclCommInitRank(&c, world, uid, rank);
   if (r != ncclSuccess) return nccl_fail(r, "ncclCommInitRank");
-  *comm = new ipm_comm{c, rank, world, device};
+  ipm_comm* m = new ipm_comm();
+  m->nccl = c;
+  m->rank = rank;
+  m->world = world;
+  m->device = device;
+  ipm_status s = setup_peer_memory(m);
+  if (s) {
+    ipm_comm_destroy(m);
+    return s;
+  }
+  *comm = m;
   return IPM_OK;
 }
 
 ipm_status ipm_comm_destroy(ipm_comm* comm) {
   if (!comm) return IPM_OK;
+  cudaDeviceSynchronize();
+  for (int q = 0; q < 64; ++q)
+    if (comm->opened[q]) cudaIpcCloseMemHandle(comm->opened[q]);
+  if (comm->peers_dev) cudaFree(comm->peers_dev);
+  if (comm->sym) cudaFree(comm->sym);
   ncclResult_t r = ncclCommDestroy(comm->nccl);
   delete comm;
   if (r != ncclSuccess) return nccl_fail(r, "ncclCommDestroy");
@@ -112,6 +192,11 @@ ipm_status ipm_reduce_dist_async(ipm_comm* comm, ipm_op op, ipm_dtype dt, const 
     return IPM_E_WORKSPACE;
   }
   cudaStream_t st = (cudaStream_t)stream;
+  if (comm->p2p && dist_mode_option() == 0) {  // one kernel: reduction + exchange over peer memory
+    DistArgs d{comm->peers_dev, comm->rank, comm->world, dist_timeout_ns()};
+    return launch_flat(op, dt, dev_shard, n_shard, scalar_bits(dt, init), init != nullptr, L_DIST, dev_result, ws,
+                       st, &d);
+  }
   uint64_t* local = (uint64_t*)((char*)ws + WS_LOCAL);
   uint64_t* slots = (uint64_t*)((char*)ws + WS_SLOTS);
   // local partial (an empty shard yields the identity: the kernel runs one CTA over nothing)
@@ -137,6 +222,26 @@ ipm_status ipm_reduce_dist(ipm_comm* comm, ipm_op op, ipm_dtype dt, const void* 
   ncclResult_t ar;
   if (ncclCommGetAsyncError(comm->nccl, &ar) == ncclSuccess && ar != ncclSuccess)
     return nccl_fail(ar, "ncclCommGetAsyncError");
+  int err = 0;
+  if (comm->p2p && ipm_comm_error(comm, &err) == IPM_OK && err) {
+    set_error("fused exchange: a peer did not arrive within the timeout (result undefined)");
+    return IPM_E_NCCL;
+  }
+  return IPM_OK;
+}
+
+int ipm_comm_uses_peer_memory(const ipm_comm* comm) { return comm && comm->p2p && dist_mode_option() == 0; }
+
+ipm_status ipm_comm_error(ipm_comm* comm, int* err) {
+  if (!comm || !err) {
+    set_error("NULL pointer");
+    return IPM_E_NULL;
+  }
+  uint64_t v = 0;
+  cudaError_t e = cudaMemcpy(&v, comm->sym + SYM_ERROR, 8, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(error word)");
+  *err = v ? 1 : 0;
+  if (v) cudaMemset(comm->sym + SYM_ERROR, 0, 8);
   return IPM_OK;
 }
 

@@ -33,9 +33,16 @@ size_t esize(ipm_dtype dt);
 uint64_t scalar_bits(ipm_dtype dt, const void* host_scalar);
 
 // kernel launchers (ipm_api.cu); all asynchronous on `st`
-enum { L_RESULT = 0, L_PARTIAL = 1, L_ACCUM_FIRST = 2, L_ACCUM = 3 };
+enum { L_RESULT = 0, L_PARTIAL = 1, L_ACCUM_FIRST = 2, L_ACCUM = 3, L_DIST = 5 };
+struct DistArgs {             // L_DIST: the fused multi-GPU exchange (ipm_kernels.cuh dist_exchange)
+  uint64_t* const* peers;     // device array of world symmetric-buffer pointers
+  int rank, world;
+  long long timeout_ns;
+};
 ipm_status launch_flat(ipm_op op, ipm_dtype dt, const void* dev, int64_t n, uint64_t init, int has_init, int mode,
-                       void* out, void* ws, cudaStream_t st);
+                       void* out, void* ws, cudaStream_t st, const DistArgs* dist = nullptr);
+int dist_mode_option();       // IPM_OPT_DIST_MODE: 0 auto (peer memory when mapped), 1 NCCL
+long long dist_timeout_ns();
 ipm_status launch_finalize(ipm_op op, ipm_dtype dt, const uint64_t* slots, int P, uint64_t init, int has_init,
                            void* out, cudaStream_t st);
 

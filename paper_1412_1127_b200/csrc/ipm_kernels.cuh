@@ -91,8 +91,79 @@ struct FlatParams {
   unsigned* tickets;      // gridDim.y tickets (unused when gridDim.x == 1); left at zero
   unsigned long long* counter;  // dynamic schedules: tile / chunk counter, left at zero
   int64_t max_chunks;     // k_flat_guided: partial slots available for dynamic chunks
+  // MODE_DIST (multi-GPU, one kernel): the CTA that finishes this rank's shard exchanges the rank partial with
+  // every peer through NVLink peer memory (see dist_exchange)
+  uint64_t* const* peers; // device array: world pointers to each rank's symmetric slot buffer (own = [rank])
+  int rank, world;
+  long long timeout_ns;
 };
-enum { MODE_RESULT = 0, MODE_PARTIAL = 1, MODE_ACCUM_FIRST = 2, MODE_ACCUM = 3, MODE_CTA_PARTIALS = 4 };
+enum { MODE_RESULT = 0, MODE_PARTIAL = 1, MODE_ACCUM_FIRST = 2, MODE_ACCUM = 3, MODE_CTA_PARTIALS = 4, MODE_DIST = 5 };
+
+// symmetric slot buffer layout (uint64 words): [parity 0..1][rank 0..63] x {value, epoch}, then the epoch
+// counter and the error flag
+constexpr int SYM_RANKS = 64;
+constexpr int SYM_EPOCH = 2 * 2 * SYM_RANKS;
+constexpr int SYM_ERROR = SYM_EPOCH + 1;
+constexpr int SYM_WORDS = SYM_EPOCH + 8;
+
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_relaxed_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ long long globaltimer_ns() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// a9 fused into the reduction kernel (one thread of the CTA that finished this rank's shard): store the rank's
+// accumulator partial into slot [parity][rank] of EVERY rank's symmetric buffer (NVLink peer stores, value then
+// epoch with release semantics), wait until all world slots of the own buffer carry this epoch (acquire), fold
+// them in rank order, merge the variable's original value and write the result. The epoch is a device-side
+// counter in the own buffer (one per call, so the kernel can be captured in a CUDA graph); two parities let a
+// fast rank start call e+1 while a slow rank still reads call e. A peer that never arrives sets the error word
+// after timeout_ns instead of hanging the GPU.
+template <class R>
+__device__ __noinline__ void dist_exchange(const FlatParams& p, typename R::A total) {
+  using A = typename R::A;
+  using B = typename R::B;
+  uint64_t* own = p.peers[p.rank];
+  const uint64_t ep = own[SYM_EPOCH] + 1;
+  own[SYM_EPOCH] = ep;
+  const int base = 2 * (int)(ep & 1u) * SYM_RANKS;
+  const uint64_t v = pack(total);
+  for (int q = 0; q < p.world; ++q) {
+    uint64_t* slot = p.peers[q] + base + 2 * p.rank;
+    st_relaxed_sys(slot, v);
+    st_release_sys(slot + 1, ep);
+  }
+  const long long t0 = globaltimer_ns();
+  bool timed_out = false;
+  for (int q = 0; q < p.world && !timed_out; ++q)
+    while (ld_acquire_sys(own + base + 2 * q + 1) != ep) {
+      if (globaltimer_ns() - t0 > p.timeout_ns) {
+        timed_out = true;
+        own[SYM_ERROR] = 1ull;
+        break;
+      }
+    }
+  A t = R::id();
+  for (int q = 0; q < p.world; ++q) t = R::op(t, unpack<A>(ld_relaxed_sys(own + base + 2 * q)));
+  if (p.has_init) t = R::op(R::lift((B)p.init), t);
+  *(B*)p.out = R::fin(t);
+}
 
 template <class R>
 __device__ __forceinline__ void store_out(const FlatParams& p, int64_t row, typename R::A total) {
@@ -107,6 +178,7 @@ __device__ __forceinline__ void store_out(const FlatParams& p, int64_t row, type
     }
     case MODE_PARTIAL: ((uint64_t*)p.out)[row] = pack(total); break;
     case MODE_ACCUM_FIRST: *(uint64_t*)p.out = pack(total); break;
+    case MODE_DIST: dist_exchange<R>(p, total); break;
     default: *(uint64_t*)p.out = pack(R::op(unpack<A>(*(uint64_t*)p.out), total)); break;
   }
 }

@@ -78,6 +78,8 @@ def _load():
         "ipm_comm_init": ([ctypes.POINTER(vp), ci, ci, vp, ci], ci),
         "ipm_comm_destroy": ([vp], ci),
         "ipm_shard_range": ([i64, ci, ci, ctypes.POINTER(i64), ctypes.POINTER(i64)], ci),
+        "ipm_comm_uses_peer_memory": ([vp], ci),
+        "ipm_comm_error": ([vp, ctypes.POINTER(ci)], ci),
         "ipm_reduce_dist": ([vp, ci, ci, vp, i64, vp, vp, vp], ci),
         "ipm_reduce_dist_async": ([vp, ci, ci, vp, i64, vp, vp, vp, vp], ci),
     }
@@ -94,7 +96,8 @@ EXPORTED = ("ipm_status_str ipm_last_error_message ipm_op_legal ipm_dtype_size i
             "ipm_present_count ipm_workspace_bytes ipm_workspace_init ipm_reduce ipm_reduce_async "
             "ipm_reduce_segmented ipm_reduce_ragged ipm_reduce_partials ipm_finalize_partials ipm_reduce_2d ipm_reduce_2d_async ipm_fused_nvars ipm_reduce_fused ipm_reduce_fused_async ipm_reduce_host ipm_release_staging ipm_set_option ipm_profile_enable ipm_profile_read "
             "ipm_profile_disable ipm_flat_geometry ipm_comm_id_bytes "
-            "ipm_comm_unique_id ipm_comm_init ipm_comm_destroy ipm_shard_range ipm_reduce_dist "
+            "ipm_comm_unique_id ipm_comm_init ipm_comm_destroy ipm_shard_range ipm_comm_uses_peer_memory ipm_comm_error "
+            "ipm_reduce_dist "
             "ipm_reduce_dist_async").split()
 
 
@@ -374,7 +377,8 @@ def identity_value(op: str, dt: int):
     return out.cpu().numpy()[0]
 
 
-OPTIONS = {"flat_ctas_per_sm": 0, "seg_kernel": 1, "deterministic": 2}
+OPTIONS = {"flat_ctas_per_sm": 0, "seg_kernel": 1, "deterministic": 2, "dist_mode": 3, "dist_timeout_ms": 4}
+DIST_MODES = {"auto": 0, "p2p": 0, "nccl": 1}
 SEG_KERNELS = {"auto": 0, "ldg": 1, "tma": 2}
 
 
@@ -383,6 +387,8 @@ def set_option(key: str, value) -> None:
     ('auto' | 'ldg' | 'tma')."""
     if key == "seg_kernel" and isinstance(value, str):
         value = SEG_KERNELS[value]
+    if key == "dist_mode" and isinstance(value, str):
+        value = DIST_MODES[value]
     _check(lib.ipm_set_option(OPTIONS[key], int(value)), "ipm_set_option")
 
 
@@ -478,6 +484,22 @@ def shard_range(n: int, rank: int, world: int):
     return lo.value, hi.value
 
 
+class _StdoutToStderr:
+    """NCCL prints its version banner on the C-level stdout during init; keep stdout for the caller's output."""
+
+    def __enter__(self):
+        import sys
+        sys.stdout.flush()
+        self._saved = os.dup(1)
+        os.dup2(2, 1)
+        return self
+
+    def __exit__(self, *exc):
+        os.dup2(self._saved, 1)
+        os.close(self._saved)
+        return False
+
+
 class Comm:
     """One NCCL communicator per process/GPU, bootstrapped through the torch.distributed store."""
 
@@ -496,8 +518,14 @@ class Comm:
         self._id = ctypes.create_string_buffer(uid, nb)
         self._h = ctypes.c_void_p()
         torch.cuda.set_device(device)
-        _check(lib.ipm_comm_init(ctypes.byref(self._h), rank, world, self._id, device), "ipm_comm_init")
+        with _StdoutToStderr():
+            _check(lib.ipm_comm_init(ctypes.byref(self._h), rank, world, self._id, device), "ipm_comm_init")
         self.rank, self.world, self.device = rank, world, device
+
+    @property
+    def fused(self) -> bool:
+        """True when reduce() exchanges partials inside the reduction kernel over peer memory (no NCCL)."""
+        return bool(lib.ipm_comm_uses_peer_memory(self._h))
 
     def close(self):
         if self._h:

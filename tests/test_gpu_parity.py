@@ -271,16 +271,52 @@ def test_data_clauses_and_host_path(ipm):
 
 # --------------------------------------------------------------------------- multi-GPU code path at world 1
 
-def test_dist_world1(ipm):
+@pytest.mark.parametrize("mode", ["p2p", "nccl"])
+def test_dist_world1(ipm, mode):
     import torch.distributed as dist
-    store = dist.HashStore()
-    comm = ipm.Comm(0, 1, torch.cuda.current_device(), store=store)
-    for op, dt in [("+", "float32"), ("^", "int64"), ("max", "float64"), ("&&", "int32")]:
-        spec = workload(op, dt, 1_000_003, seed=2)
-        x = device_input(spec)
-        got = comm.reduce(op, x, init=NPT[dt](1))
-        want_t, want_ld = oracle.reduce(op, ipmgen.fill_host(spec), init=NPT[dt](1))
-        check(op, dt, got, want_t, want_ld)
+    ipm.set_option("dist_mode", mode)
+    try:
+        comm = ipm.Comm(0, 1, torch.cuda.current_device(), store=dist.HashStore())
+        assert comm.fused == (mode == "p2p")
+        for op, dt in [("+", "float32"), ("^", "int64"), ("max", "float64"), ("&&", "int32"), ("*", "float64"),
+                       ("min", "int32")]:
+            spec = workload(op, dt, 1_000_003, seed=2)
+            x = device_input(spec)
+            want_t, want_ld = oracle.reduce(op, ipmgen.fill_host(spec), init=NPT[dt](1))
+            for _ in range(3):  # repeated calls: the fused path's epochs / parities
+                check(op, dt, comm.reduce(op, x, init=NPT[dt](1)), want_t, want_ld)
+            # back-to-back asynchronous calls, then one sync
+            outs = [comm.reduce_async(op, x, init=NPT[dt](1)) for _ in range(5)]
+            for o in outs:
+                check(op, dt, o.cpu().numpy()[0], want_t, want_ld)
+            # an empty shard contributes the identity
+            check(op, dt, comm.reduce(op, x[:0], init=NPT[dt](1)), *oracle.reduce(op, x[:0].cpu().numpy(),
+                                                                                 init=NPT[dt](1)))
+        comm.close()
+    finally:
+        ipm.set_option("dist_mode", "auto")
+
+
+def test_dist_fused_graph_capture(ipm):
+    import torch.distributed as dist
+    comm = ipm.Comm(0, 1, torch.cuda.current_device(), store=dist.HashStore())
+    spec = ipmgen.Spec("float32", 3_000_017, "random", seed=5)
+    x = device_input(spec)
+    s = torch.cuda.Stream()
+    ws = torch.zeros(ipm.WS_BYTES, dtype=torch.uint8, device="cuda")
+    out = torch.empty(1, dtype=torch.float32, device="cuda")
+    with torch.cuda.stream(s):
+        comm.reduce_async("+", x, out=out, ws=ws, stream=s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        comm.reduce_async("+", x, out=out, ws=ws, stream=s)
+    _, want = oracle.reduce("+", ipmgen.fill_host(spec))
+    for _ in range(4):  # the device-side epoch advances on every replay
+        out.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        check("+", "float32", out.cpu().numpy()[0], None, want)
     comm.close()
 
 
