@@ -865,6 +865,186 @@ __global__ void __launch_bounds__(WARPS * 32) k_ragged(RaggedParams p) {
   }
 }
 
+// Element-parallel variant of k_ragged (same ranges, same head/tail records, same fix-up): the warp streams
+// its element range in chunks of 32 lanes x VW contiguous elements (one 32-byte vector per lane), marks the
+// positions where rows start (from a window of 32 row offsets, through a per-warp shared-memory map
+// position -> row), folds each lane's VW elements with those breaks, and joins the pieces of rows that cross
+// lanes and chunks with a segmented warp scan. Every element is read once with coalesced vector loads
+// whatever the row lengths (short rows no longer cost a warp each).
+template <class A>
+__device__ __forceinline__ A shfl_up_acc(A v, int d) {
+  return unpack<A>(__shfl_up_sync(FULL, pack(v), d));
+}
+template <class A>
+__device__ __forceinline__ A shfl_acc(A v, int src) {
+  return unpack<A>(__shfl_sync(FULL, pack(v), src));
+}
+
+template <class R, int WARPS, int MINB, int VPL>
+__global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_vec(RaggedParams p) {
+  using B = typename R::B;
+  using A = typename R::A;
+  using VT = typename Vec<B>::T;
+  constexpr int VW = Vec<B>::W;
+  constexpr int EPL = VW * VPL;  // elements per lane per chunk (<= 32: one flag bit each)
+  constexpr int CH = 32 * EPL;   // elements per chunk
+  static_assert(EPL <= 32, "flag word");
+  __shared__ long long s_rid[WARPS][CH];  // chunk position -> row starting there (valid where flagged)
+  __shared__ unsigned s_flag[WARPS][32];  // per lane: bit k = a row starts at the lane's element k
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  long long* rid_map = s_rid[wid];
+  unsigned* flagw = s_flag[wid];
+  flagw[lane] = 0u;
+  const unsigned lanemask_lt = (1u << lane) - 1u;
+  const int64_t w = (int64_t)blockIdx.x * WARPS + wid;
+  const int64_t nw = (int64_t)gridDim.x * WARPS;
+  const B* a = (const B*)p.a;
+  const int64_t P0 = __ldg(p.off), P1 = __ldg(p.off + p.rows);
+  const int64_t nnz = P1 - P0;
+  const int64_t lo = P0 + (int64_t)(((__int128)nnz * w) / nw);
+  const int64_t hi = P0 + (int64_t)(((__int128)nnz * (w + 1)) / nw);
+  const bool last = (w == nw - 1);
+  const int64_t r0 = warp_lower_bound(p.off, p.rows, lo);
+  const int64_t hrow = (r0 > 0 && lo < hi && __ldg(p.off + r0 - 1) < lo && __ldg(p.off + r0) > lo) ? r0 - 1 : -1;
+  if (lane == 0) {
+    p.head_row[w] = lo < hi ? -1 : -2;
+    p.tail_row[w] = -1;
+  }
+  auto finish = [&](int64_t row, A v) {  // a complete row owned by this warp
+    if (p.has_init) v = R::op(R::lift((B)p.init), v);
+    ((B*)p.out)[row] = R::fin(v);
+  };
+  // window of row offsets: lane l holds off[wb + l] and off[wb + l + 1]
+  int64_t wb = r0;
+  auto load_window = [&](int64_t base, int64_t& s0, int64_t& e0) {
+    const int64_t r = base + lane;
+    s0 = r <= p.rows ? __ldg(p.off + r) : P1;
+    e0 = r + 1 <= p.rows ? __ldg(p.off + r + 1) : P1;
+  };
+  int64_t sw, ew;
+  load_window(wb, sw, ew);
+  int64_t open_rid = hrow;
+  A open_val = R::id();
+  __syncwarp();
+  if (lo < hi) {
+    // chunk bases: positions whose address is 32-byte aligned
+    const int64_t q0 = lo - (int64_t)(((uintptr_t)(a + lo) & 31u) / sizeof(B));
+    for (int64_t Bc = q0; Bc < hi; Bc += CH) {
+      // this lane's elements, issued first: positions Bc + EPL*lane + k
+      const int64_t p0 = Bc + (int64_t)EPL * lane;
+      B x[EPL];
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        const int64_t pv = p0 + v * VW;
+        if (pv >= lo && pv + VW <= hi) {
+          const VT t = ldv((const VT*)(a + pv));
+#pragma unroll
+          for (int k = 0; k < VW; ++k) x[v * VW + k] = t.w[k];
+        } else {
+#pragma unroll
+          for (int k = 0; k < VW; ++k) x[v * VW + k] = (pv + k >= lo && pv + k < hi) ? lds(a + pv + k) : (B)0;
+        }
+      }
+      const int64_t cl = Bc > lo ? Bc : lo, ch = Bc + CH < hi ? Bc + CH : hi;  // valid positions [cl, ch)
+      // rows starting in [cl, ch): flag their start position; empty ones are finished here
+      while (true) {
+        const int64_t r = wb + lane;
+        const bool inr = r < p.rows && sw >= cl && sw < ch;
+        if (inr && ew > sw) {
+          const int rel = (int)(sw - Bc);
+          rid_map[rel] = r;
+          atomicOr(&flagw[rel / EPL], 1u << (rel % EPL));
+        }
+        if (inr && ew == sw) finish(r, R::id());
+        const bool done = r >= p.rows || sw < ch;
+        if (__all_sync(FULL, done) && wb + 32 < p.rows) {
+          wb += 32;
+          load_window(wb, sw, ew);
+          continue;
+        }
+        break;
+      }
+      __syncwarp();
+      const unsigned fl = flagw[lane];
+      flagw[lane] = 0u;
+      const int rlo = (int)(lo > p0 ? (lo - p0 < EPL ? lo - p0 : EPL) : 0);  // valid k in [rlo, rhi)
+      const int rhi = (int)(hi > p0 ? (hi - p0 < EPL ? hi - p0 : EPL) : 0);
+      // lane-local fold with row breaks: head = before the first flag, tail = from the last flag
+      A head = R::id(), cur = R::id();
+      int lastk = -1;
+#pragma unroll
+      for (int k = 0; k < EPL; ++k) {
+        const A xv = (k >= rlo && k < rhi) ? R::lift(x[k]) : R::id();
+        if ((fl >> k) & 1u) {
+          if (lastk >= 0) finish(rid_map[EPL * lane + lastk], cur);  // a whole row inside this lane
+          else head = cur;
+          cur = xv;
+          lastk = k;
+        } else {
+          cur = R::op(cur, xv);
+        }
+      }
+      const bool flag = fl != 0u;
+      if (!flag) head = cur;
+      const long long my_rid = flag ? rid_map[EPL * lane + lastk] : -1;
+      // segmented inclusive scan over lanes: a flagged lane starts a segment with its tail value
+      const unsigned bal = __ballot_sync(FULL, flag);
+      const unsigned le = bal & (lanemask_lt | (1u << lane));
+      const int start = le ? 31 - __clz(le) : 0;
+      A sv = flag ? cur : head;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const A ov = shfl_up_acc(sv, d);
+        if (lane - d >= start) sv = R::op(ov, sv);
+      }
+      // the row open at this lane's start
+      const unsigned lt = bal & lanemask_lt;
+      A ev = shfl_up_acc(sv, 1);
+      const int src = lt ? 31 - __clz(lt) : 0;
+      const long long rr = __shfl_sync(FULL, my_rid, src);
+      if (!lt) ev = lane == 0 ? open_val : R::op(open_val, ev);
+      const long long er = lt ? rr : open_rid;
+      if (flag && er >= 0) {  // it ends at this lane's first flag
+        const A v = R::op(ev, head);
+        if (er == hrow) {
+          p.head_row[w] = hrow;
+          p.head_part[w] = pack(v);
+        } else {
+          finish(er, v);
+        }
+      }
+      // carry into the next chunk: the row open at the end of lane 31
+      const A lv = shfl_acc(sv, 31);
+      const long long lr = __shfl_sync(FULL, my_rid, bal ? 31 - __clz(bal) : 0);
+      if (bal) {
+        open_val = lv;
+        open_rid = lr;
+      } else {
+        open_val = R::op(open_val, lv);
+      }
+      __syncwarp();
+    }
+  }
+  // the row still open at hi
+  if (lane == 0 && open_rid >= 0) {
+    if (open_rid == hrow) {
+      p.head_row[w] = hrow;
+      p.head_part[w] = pack(open_val);
+    } else if (__ldg(p.off + open_rid + 1) <= hi) {
+      finish(open_rid, open_val);
+    } else {
+      p.tail_row[w] = open_rid;
+      p.tail_part[w] = pack(open_val);
+    }
+  }
+  // the last warp also owns the empty rows that start at P1 (after every element)
+  if (last) {
+    const int64_t r = warp_lower_bound(p.off, p.rows, lo < hi ? P1 : lo);
+    for (int64_t q = r + lane; q < p.rows; q += 32)
+      if (__ldg(p.off + q) == __ldg(p.off + q + 1)) finish(q, R::id());
+  }
+}
+
 // one warp per phase-1 warp: a warp with a TAIL record finishes that row by folding the HEAD records of the
 // following warps (in warp order, 32 at a time with a fixed lane tree) while they continue the same row
 template <class R>
