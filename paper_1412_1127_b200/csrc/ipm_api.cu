@@ -174,13 +174,7 @@ struct Launch {
     k_seg_warp<R, SEG_WARPS, SEG_U><<<grid, SEG_WARPS * 32, 0, st>>>(p);
   }
   static void ragged(const RaggedParams& p, int blocks, int64_t nw, cudaStream_t st) {
-    static const int cfg = env_int("IPM_RAGGED_CFG", 0);
-    switch (cfg) {
-      case 1: k_ragged_vec<R, 8, 4, 1><<<blocks, 256, 0, st>>>(p); break;
-      case 2: k_ragged_vec<R, 8, 3, 2><<<blocks, 256, 0, st>>>(p); break;
-      case 3: k_ragged_vec<R, 8, 2, 2><<<blocks, 256, 0, st>>>(p); break;
-      default: k_ragged_vec<R, 8, 4, 2><<<blocks, 256, 0, st>>>(p); break;
-    }
+    k_ragged_vec<R, 8, 4, 2><<<blocks, 256, 0, st>>>(p);  // 4 CTAs x 8 warps per SM, 2 vectors per lane
     k_ragged_fix<R><<<(unsigned)((nw + 7) / 8), 256, 0, st>>>(p, nw);
   }
   static void two_d(const Params2D& q, int grid, cudaStream_t st) {
@@ -707,9 +701,7 @@ ipm_status ipm_reduce_ragged(ipm_op op, ipm_dtype dt, const void* dev, const int
   p.init = scalar_bits(dt, init);
   p.has_init = init != nullptr;
   p.out = dev_out;
-  static const int cfg = env_int("IPM_RAGGED_CFG", 0);
-  const int cps = cfg == 3 ? 2 : cfg == 2 ? 3 : 4;  // CTAs of 8 warps per SM
-  const int64_t nw = std::min<int64_t>((int64_t)sm_count() * 8 * cps, WS_MAX_RAGGED_WARPS);
+  const int64_t nw = std::min<int64_t>((int64_t)sm_count() * 32, WS_MAX_RAGGED_WARPS);  // 4 CTAs x 8 warps per SM
   int64_t* base = (int64_t*)((char*)ws + WS_RAGGED);
   p.head_row = base;
   p.head_part = (uint64_t*)(base + WS_MAX_RAGGED_WARPS);
