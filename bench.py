@@ -280,6 +280,13 @@ def suite(ipm, torch, ipmgen, peak):
     return out
 
 
+def ctypes_err(ipm, comm):
+    import ctypes
+    e = ctypes.c_int(0)
+    ipm.lib.ipm_comm_error(comm._h, ctypes.byref(e))
+    return e.value
+
+
 def run_ours(args, rank, world, local_rank):
     import numpy as np
     import torch
@@ -304,6 +311,19 @@ def run_ours(args, rank, world, local_rank):
     ipmgen.fill_device(spec, x.data_ptr(), lo, n_shard, torch.cuda.current_stream().cuda_stream)
     comm = ipm.Comm(rank, world, dev, store=store)
     comm_fused = comm.fused
+    if comm_fused and world > 1:
+        # probe the fused peer-memory exchange once with a short timeout; fall back to NCCL everywhere if any rank
+        # saw a peer time out (every rank must take the same path)
+        ipm.set_option("dist_timeout_ms", 5000)
+        probe = torch.ones(1024, dtype=torch.float32, device="cuda")
+        got = comm.reduce_async("+", probe).cpu().numpy()[0]
+        err = ctypes_err(ipm, comm)
+        bad = torch.tensor([int(err or got != 1024.0 * world)], device="cuda")
+        dist.all_reduce(bad, op=dist.ReduceOp.MAX)
+        ipm.set_option("dist_timeout_ms", 30000)
+        if bad.item():
+            ipm.set_option("dist_mode", "nccl")
+            comm_fused = False
     ws = ipm.workspace()
     out = torch.empty(1, dtype=torch.float32, device="cuda")
     init = np.float32(0.0)
@@ -314,13 +334,13 @@ def run_ours(args, rank, world, local_rank):
             dist.barrier()
         torch.cuda.synchronize()
 
-    # clock spin-up (setup, untimed): back-to-back steps for >= 0.25 s so the timed steps run at steady clocks
-    t_spin = time.perf_counter()
-    spin = 0
-    while time.perf_counter() - t_spin < 0.25:
+    # clock spin-up (setup, untimed): ~0.25 s of back-to-back steps so the timed steps run at steady clocks.
+    # The count is a function of the shard size only, identical on every rank (every call is collective).
+    spin = max(3, int(0.25 / (n_shard * ELEM / 7.0e12)))
+    spin = min(spin, 2000)
+    for _ in range(spin):
         comm.reduce_async("+", x, init=init, out=out, ws=ws)
-        torch.cuda.synchronize()
-        spin += 1
+    torch.cuda.synchronize()
     for _ in range(args.warmup):
         comm.reduce_async("+", x, init=init, out=out, ws=ws)
     barrier()
@@ -346,6 +366,11 @@ def run_ours(args, rank, world, local_rank):
     step_ms = [a.elapsed_time(b) for a, b in step_ev]
     kern_ms = [m for m, k in zip(kt.ms, kt.kinds) if k == 0]
     result = float(out.item())
+    ranks_agree = True
+    if world > 1:
+        allr = [None] * world
+        dist.all_gather_object(allr, out.cpu().numpy().tobytes())
+        ranks_agree = all(r == allr[0] for r in allr)
 
     total_bytes = N_TOTAL * ELEM
     value = total_bytes / (ms_step / 1e3) / 1e9  # whole-job GB/s
@@ -429,6 +454,7 @@ def run_ours(args, rank, world, local_rank):
                                   if comm_fused else "per step: 1 k_flat_guided + 1 k_finalize (plus NCCL's own "
                                   "AllGather kernel)"),
             "clocks": clk.summary(), "result_rank0": result, "spinup_steps": spin,
+            "ranks_agree": ranks_agree,
         }
         if st is not None:
             line["suite"] = st

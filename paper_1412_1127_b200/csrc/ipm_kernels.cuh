@@ -772,100 +772,7 @@ __device__ __forceinline__ int64_t warp_lower_bound(const int64_t* off, int64_t 
   return ge ? lo + (__ffs(ge) - 1) : hi;
 }
 
-// the lanes' private fold of a[s..e) (not yet combined across lanes)
-template <class R>
-__device__ __forceinline__ typename R::A warp_fold_range(const typename R::B* a, int64_t s, int64_t e) {
-  using B = typename R::B;
-  using A = typename R::A;
-  using VT = typename Vec<B>::T;
-  constexpr int VW = Vec<B>::W;
-  const int lane = threadIdx.x & 31;
-  A acc = R::id();
-  if (e - s >= 4 * 32 * VW) {  // long segment: 32-byte vectors with a head/tail peel
-    const B* p = a + s;
-    int64_t head = (int64_t)(((32u - ((uintptr_t)p & 31u)) & 31u) / sizeof(B));
-    const int64_t n = e - s;
-    const int64_t nv = (n - head) / VW;
-    const int64_t tail0 = head + nv * VW;
-    const VT* vp = (const VT*)(p + head);
-    A v2[2] = {R::id(), R::id()};
-    int64_t i = lane;
-    for (; i + 32 < nv; i += 64) {
-      const VT x0 = ldv(vp + i), x1 = ldv(vp + i + 32);
-#pragma unroll
-      for (int k = 0; k < VW; ++k) {
-        v2[0] = R::op(v2[0], R::lift(x0.w[k]));
-        v2[1] = R::op(v2[1], R::lift(x1.w[k]));
-      }
-    }
-    for (; i < nv; i += 32) {
-      const VT x0 = ldv(vp + i);
-#pragma unroll
-      for (int k = 0; k < VW; ++k) v2[0] = R::op(v2[0], R::lift(x0.w[k]));
-    }
-    if (lane < head) v2[1] = R::op(v2[1], R::lift(lds(p + lane)));
-    if (lane < n - tail0) v2[1] = R::op(v2[1], R::lift(lds(p + tail0 + lane)));
-    acc = R::op(v2[0], v2[1]);
-  } else {
-    for (int64_t j = s + lane; j < e; j += 32) acc = R::op(acc, R::lift(lds(a + j)));
-  }
-  return acc;
-}
-
-template <class R, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32) k_ragged(RaggedParams p) {
-  using B = typename R::B;
-  using A = typename R::A;
-  const int lane = threadIdx.x & 31;
-  const int64_t w = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5);
-  const int64_t nw = (int64_t)gridDim.x * WARPS;
-  const B* a = (const B*)p.a;
-  const int64_t P0 = __ldg(p.off), P1 = __ldg(p.off + p.rows);
-  const int64_t nnz = P1 - P0;
-  const int64_t lo = P0 + (int64_t)(((__int128)nnz * w) / nw);
-  const int64_t hi = P0 + (int64_t)(((__int128)nnz * (w + 1)) / nw);
-  const bool last = (w == nw - 1);
-  int64_t r = warp_lower_bound(p.off, p.rows, lo);  // first row starting at or after lo
-  // head: the row that started before lo and still has elements at lo (-2: this warp's range is empty and
-  // transparent to the fix-up walk, which happens when nnz < nw)
-  int64_t hrow = lo < hi ? -1 : -2;
-  A hpart = R::id();
-  if (r > 0 && lo < hi) {
-    const int64_t prev_end = r <= p.rows ? __ldg(p.off + r) : P1;
-    if (__ldg(p.off + r - 1) < lo && prev_end > lo) {
-      hrow = r - 1;
-      hpart = R::warp(warp_fold_range<R>(a, lo, min(prev_end, hi)));
-    }
-  }
-  // owned rows: off[r] in [lo, hi) (the last warp also owns the empty rows that start at P1)
-  int64_t trow = -1;
-  A tpart = R::id();
-  while (r < p.rows) {
-    const int64_t s = __ldg(p.off + r);
-    if (!(s < hi || (last && s == P1))) break;
-    const int64_t e = __ldg(p.off + r + 1);
-    A t = R::warp(warp_fold_range<R>(a, s, min(e, hi)));
-    if (e <= hi) {
-      if (lane == 0) {
-        if (p.has_init) t = R::op(R::lift((B)p.init), t);
-        ((B*)p.out)[r] = R::fin(t);
-      }
-    } else {
-      trow = r;
-      tpart = t;
-      break;  // a row running past hi is the last row this warp owns
-    }
-    ++r;
-  }
-  if (lane == 0) {
-    p.head_row[w] = hrow;
-    p.head_part[w] = pack(hpart);
-    p.tail_row[w] = trow;
-    p.tail_part[w] = pack(tpart);
-  }
-}
-
-// Element-parallel variant of k_ragged (same ranges, same head/tail records, same fix-up): the warp streams
+// Phase 1 (k_ragged_vec, element-parallel): the warp streams
 // its element range in chunks of 32 lanes x VW contiguous elements (one 32-byte vector per lane), marks the
 // positions where rows start (from a window of 32 row offsets, through a per-warp shared-memory map
 // position -> row), folds each lane's VW elements with those breaks, and joins the pieces of rows that cross
