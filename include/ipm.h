@@ -246,6 +246,10 @@ size_t ipm_comm_id_bytes(void);
 ipm_status ipm_comm_unique_id(void* id_out);
 ipm_status ipm_comm_init(ipm_comm** comm, int rank, int world, const void* id, int device);
 ipm_status ipm_comm_destroy(ipm_comm* comm);
+/* `world` ranks in ONE process on ONE device (comms[0..world-1]), exchanging through each other's slot buffers
+ * with the fused path only (no NCCL). Each rank's calls go on its own stream with its own workspace; the ranks'
+ * kernels then run concurrently on the device. Used to exercise the multi-rank exchange on a single GPU. */
+ipm_status ipm_comm_init_group(ipm_comm** comms, int world, int device);
 ipm_status ipm_shard_range(int64_t n, int rank, int world, int64_t* lo, int64_t* hi);
 /* dev_shard: this rank's n_shard elements (device); inout: host scalar, the same init on every rank (in),
  * the global result (out). Blocks until *inout is written. */

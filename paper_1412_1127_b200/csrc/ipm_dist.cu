@@ -139,6 +139,43 @@ ipm_status ipm_comm_init(ipm_comm** comm, int rank, int world, const void* id, i
   return IPM_OK;
 }
 
+ipm_status ipm_comm_init_group(ipm_comm** comms, int world, int device) {
+  if (!comms) {
+    set_error("NULL pointer");
+    return IPM_E_NULL;
+  }
+  if (world < 1 || world > WS_MAX_RANKS) {
+    set_error("world out of range (1..64)");
+    return IPM_E_ARG;
+  }
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  uint64_t* ptrs[64] = {nullptr};
+  for (int q = 0; q < world; ++q) {
+    ipm_comm* m = new ipm_comm();
+    m->nccl = nullptr;
+    m->rank = q;
+    m->world = world;
+    m->device = device;
+    m->p2p = 1;
+    comms[q] = m;
+    if ((e = cudaMalloc(&m->sym, SYM_BYTES)) != cudaSuccess || (e = cudaMemset(m->sym, 0, SYM_BYTES)) != cudaSuccess) {
+      for (int k = 0; k <= q; ++k) ipm_comm_destroy(comms[k]);
+      return cuda_fail(e, "cudaMalloc(sym)");
+    }
+    ptrs[q] = m->sym;
+  }
+  for (int q = 0; q < world; ++q) {
+    ipm_comm* m = comms[q];
+    if ((e = cudaMalloc(&m->peers_dev, sizeof(uint64_t*) * world)) != cudaSuccess ||
+        (e = cudaMemcpy(m->peers_dev, ptrs, sizeof(uint64_t*) * world, cudaMemcpyHostToDevice)) != cudaSuccess) {
+      for (int k = 0; k < world; ++k) ipm_comm_destroy(comms[k]);
+      return cuda_fail(e, "peers");
+    }
+  }
+  return IPM_OK;
+}
+
 ipm_status ipm_comm_destroy(ipm_comm* comm) {
   if (!comm) return IPM_OK;
   cudaDeviceSynchronize();
@@ -146,7 +183,7 @@ ipm_status ipm_comm_destroy(ipm_comm* comm) {
     if (comm->opened[q]) cudaIpcCloseMemHandle(comm->opened[q]);
   if (comm->peers_dev) cudaFree(comm->peers_dev);
   if (comm->sym) cudaFree(comm->sym);
-  ncclResult_t r = ncclCommDestroy(comm->nccl);
+  ncclResult_t r = comm->nccl ? ncclCommDestroy(comm->nccl) : ncclSuccess;
   delete comm;
   if (r != ncclSuccess) return nccl_fail(r, "ncclCommDestroy");
   return IPM_OK;
@@ -192,7 +229,7 @@ ipm_status ipm_reduce_dist_async(ipm_comm* comm, ipm_op op, ipm_dtype dt, const 
     return IPM_E_WORKSPACE;
   }
   cudaStream_t st = (cudaStream_t)stream;
-  if (comm->p2p && dist_mode_option() == 0) {  // one kernel: reduction + exchange over peer memory
+  if (comm->p2p && (dist_mode_option() == 0 || !comm->nccl)) {  // one kernel: reduction + exchange
     DistArgs d{comm->peers_dev, comm->rank, comm->world, dist_timeout_ns()};
     return launch_flat(op, dt, dev_shard, n_shard, scalar_bits(dt, init), init != nullptr, L_DIST, dev_result, ws,
                        st, &d);
@@ -220,7 +257,7 @@ ipm_status ipm_reduce_dist(ipm_comm* comm, ipm_op op, ipm_dtype dt, const void* 
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "ipm_reduce_dist");
   ncclResult_t ar;
-  if (ncclCommGetAsyncError(comm->nccl, &ar) == ncclSuccess && ar != ncclSuccess)
+  if (comm->nccl && ncclCommGetAsyncError(comm->nccl, &ar) == ncclSuccess && ar != ncclSuccess)
     return nccl_fail(ar, "ncclCommGetAsyncError");
   int err = 0;
   if (comm->p2p && ipm_comm_error(comm, &err) == IPM_OK && err) {
@@ -230,7 +267,9 @@ ipm_status ipm_reduce_dist(ipm_comm* comm, ipm_op op, ipm_dtype dt, const void* 
   return IPM_OK;
 }
 
-int ipm_comm_uses_peer_memory(const ipm_comm* comm) { return comm && comm->p2p && dist_mode_option() == 0; }
+int ipm_comm_uses_peer_memory(const ipm_comm* comm) {
+  return comm && comm->p2p && (dist_mode_option() == 0 || !comm->nccl);
+}
 
 ipm_status ipm_comm_error(ipm_comm* comm, int* err) {
   if (!comm || !err) {

@@ -77,6 +77,7 @@ def _load():
         "ipm_comm_unique_id": ([vp], ci),
         "ipm_comm_init": ([ctypes.POINTER(vp), ci, ci, vp, ci], ci),
         "ipm_comm_destroy": ([vp], ci),
+        "ipm_comm_init_group": ([vp, ci, ci], ci),
         "ipm_shard_range": ([i64, ci, ci, ctypes.POINTER(i64), ctypes.POINTER(i64)], ci),
         "ipm_comm_uses_peer_memory": ([vp], ci),
         "ipm_comm_error": ([vp, ctypes.POINTER(ci)], ci),
@@ -96,7 +97,7 @@ EXPORTED = ("ipm_status_str ipm_last_error_message ipm_op_legal ipm_dtype_size i
             "ipm_present_count ipm_workspace_bytes ipm_workspace_init ipm_reduce ipm_reduce_async "
             "ipm_reduce_segmented ipm_reduce_ragged ipm_reduce_partials ipm_finalize_partials ipm_reduce_2d ipm_reduce_2d_async ipm_fused_nvars ipm_reduce_fused ipm_reduce_fused_async ipm_reduce_host ipm_release_staging ipm_set_option ipm_profile_enable ipm_profile_read "
             "ipm_profile_disable ipm_flat_geometry ipm_comm_id_bytes "
-            "ipm_comm_unique_id ipm_comm_init ipm_comm_destroy ipm_shard_range ipm_comm_uses_peer_memory ipm_comm_error "
+            "ipm_comm_unique_id ipm_comm_init ipm_comm_destroy ipm_comm_init_group ipm_shard_range ipm_comm_uses_peer_memory ipm_comm_error "
             "ipm_reduce_dist "
             "ipm_reduce_dist_async").split()
 
@@ -502,6 +503,20 @@ class _StdoutToStderr:
 
 class Comm:
     """One NCCL communicator per process/GPU, bootstrapped through the torch.distributed store."""
+
+    @classmethod
+    def group(cls, world: int, device: int | None = None) -> list["Comm"]:
+        """`world` ranks in this process on one device (ipm_comm_init_group): fused exchange only."""
+        device = torch.cuda.current_device() if device is None else device
+        arr = (ctypes.c_void_p * world)()
+        _check(lib.ipm_comm_init_group(arr, world, device), "ipm_comm_init_group")
+        out = []
+        for r in range(world):
+            c = cls.__new__(cls)
+            c._h = ctypes.c_void_p(arr[r])
+            c.rank, c.world, c.device = r, world, device
+            out.append(c)
+        return out
 
     def __init__(self, rank: int, world: int, device: int, store=None, key: str = "ipm_nccl_id"):
         nb = lib.ipm_comm_id_bytes()

@@ -1,6 +1,9 @@
 """GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element on the same seeded
 inputs. Bit-exact for integer, bitwise, logical, max and min; |g - o| <= tol*|o| for float + and * with
 tol = 1e-5 (float32) / 1e-12 (float64) against the oracle's long double value (BASELINE.json north_star)."""
+import ctypes
+import time
+
 import numpy as np
 import pytest
 import torch
@@ -434,3 +437,39 @@ def test_nondeterministic_mode_parity(ipm):
                 check("+", dt, ipm.reduce("+", x), want_t, want_ld)
     finally:
         ipm.set_option("deterministic", 1)
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_dist_fused_multirank_one_gpu(ipm, world):
+    """world ranks in one process on one GPU (ipm_comm_init_group): each rank's kernel runs on its own stream and
+    exchanges its partial through the other ranks' slot buffers — the fused multi-GPU code path with world > 1."""
+    comms = ipm.Comm.group(world)
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    wss = [torch.zeros(ipm.WS_BYTES, dtype=torch.uint8, device="cuda") for _ in range(world)]
+    for op, dt, n in [("+", "float32", 10_000_019), ("^", "int64", 1_000_003), ("max", "float64", 777),
+                      ("&&", "int32", 5), ("min", "int32", 0)]:
+        spec = workload(op, dt, n, seed=world)
+        x = device_input(spec)
+        torch.cuda.synchronize()
+        h = ipmgen.fill_host(spec)
+        for rep in range(3):  # repeated, back-to-back asynchronous calls per rank (epochs / parities)
+            init = NPT[dt](rep + 1)  # a different init per call: a stale slot would give a wrong result
+            want_t, want_ld = oracle.reduce(op, h, init=init)
+            outs = []
+            t0 = time.perf_counter()
+            for r, c in enumerate(comms):
+                lo, hi = ipm.shard_range(n, r, world)
+                with torch.cuda.stream(streams[r]):
+                    o = torch.empty(1, dtype=TD[dt], device="cuda")
+                    outs.append(c.reduce_async(op, x[lo:hi], init=init, out=o, ws=wss[r], stream=streams[r]))
+            torch.cuda.synchronize()
+            assert time.perf_counter() - t0 < 2.0                    # no rank waited for a timeout
+            for c in comms:
+                e = ctypes.c_int(0)
+                ipm.lib.ipm_comm_error(c._h, ctypes.byref(e))
+                assert e.value == 0
+            vals = [o.cpu().numpy()[0] for o in outs]
+            assert len({bits(v, dt) for v in vals}) == 1, vals      # every rank gets the same bits
+            check(op, dt, vals[0], want_t, want_ld)
+    for c in comms:
+        c.close()
