@@ -92,6 +92,80 @@ void run_guided(const char* name, void* buf, size_t bytes, void* ws, int sms) {
   printf("guided %-8s B= 256 U=4 cps=4 grid=%5d  %7.3f ms  %7.1f GB/s\n", name, grid, ms, bytes / ms / 1e6);
 }
 
+// experiment: the flat clause fed by TMA bulk copies (1 persistent CTA per SM, S-stage ring of CHB bytes,
+// one producer thread, all 256 threads consume from shared memory); full tiles only (the sweep sizes are
+// multiples of the tile)
+template <class R, int S, int CHB, int NT = 256, int MINB = 1, int WAIT = 0>
+__global__ void __launch_bounds__(NT, MINB) k_flat_tma(const void* a, int64_t nbytes, uint64_t* out) {
+  using B = typename R::B;
+  using A = typename R::A;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* bar = (uint64_t*)(smem + (size_t)S * CHB);
+  __shared__ A sm[NT / 32];
+  const int64_t ntiles = nbytes / CHB;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < S; ++i) mbar_init(bar + i, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  const int64_t my = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;  // tiles b, b+G, ...
+  auto issue = [&](int64_t i) {
+    const int st = (int)(i % S);
+    const int64_t t = blockIdx.x + i * gridDim.x;
+    mbar_expect_tx(bar + st, CHB);
+    bulk_g2s(smem + (size_t)st * CHB, (const char*)a + t * CHB, CHB, bar + st);
+  };
+  if (threadIdx.x == 0)
+    for (int64_t i = 0; i < S && i < my; ++i) issue(i);
+  constexpr int EPV = 16 / sizeof(B);
+  A acc[EPV];
+#pragma unroll
+  for (int k = 0; k < EPV; ++k) acc[k] = R::id();
+  for (int64_t i = 0; i < my; ++i) {
+    const int st = (int)(i % S);
+    if (WAIT == 0) {
+      mbar_wait(bar + st, (uint32_t)((i / S) & 1));
+    } else if (WAIT == 1) {
+      if ((threadIdx.x & 31) == 0) mbar_wait(bar + st, (uint32_t)((i / S) & 1));
+      __syncwarp();
+    } else {
+      if (threadIdx.x == 0) mbar_wait(bar + st, (uint32_t)((i / S) & 1));
+      __syncthreads();
+    }
+    const unsigned char* c = smem + (size_t)st * CHB;
+#pragma unroll 4
+    for (int o = threadIdx.x * 16; o < CHB; o += NT * 16) {
+      const uint4 q = *(const uint4*)(c + o);
+      if (EPV == 4) {
+        acc[0] = R::op(acc[0], R::lift((B)q.x));
+        acc[1 % EPV] = R::op(acc[1 % EPV], R::lift((B)q.y));
+        acc[2 % EPV] = R::op(acc[2 % EPV], R::lift((B)q.z));
+        acc[3 % EPV] = R::op(acc[3 % EPV], R::lift((B)q.w));
+      } else {
+        acc[0] = R::op(acc[0], R::lift((B)(((uint64_t)q.y << 32) | q.x)));
+        acc[1 % EPV] = R::op(acc[1 % EPV], R::lift((B)(((uint64_t)q.w << 32) | q.z)));
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && i + S < my) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(i + S);
+    }
+  }
+#pragma unroll
+  for (int k = 1; k < EPV; ++k) acc[0] = R::op(acc[0], acc[k]);
+  A t = block_reduce<R, NT>(acc[0], sm);
+  if (threadIdx.x == 0) out[blockIdx.x] = pack(t);
+}
+
+template <class R, int S, int CHB, int NT = 256, int CPS = 1, int WAIT = 0>
+void run_flat_tma(const char* name, void* buf, size_t bytes, void* ws, int sms) {
+  constexpr int smem = S * CHB + S * 8;
+  CK(cudaFuncSetAttribute(k_flat_tma<R, S, CHB, NT, CPS, WAIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  float ms = time_ms([&] { k_flat_tma<R, S, CHB, NT, CPS, WAIT><<<sms * CPS, NT, smem>>>(buf, (int64_t)bytes, (uint64_t*)((char*)ws + 8192)); }, 20);
+  CK(cudaGetLastError());
+  printf("tmaflat %-7s S=%2d CHB=%6d NT=%d cps=%d W=%d  %7.3f ms  %7.1f GB/s\n", name, S, CHB, NT, CPS, WAIT, ms, bytes / ms / 1e6);
+}
+
 int main(int argc, char** argv) {
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
@@ -196,6 +270,32 @@ int main(int argc, char** argv) {
         run_guided<Red<IPM_MAX, IPM_F32>>("f32max", buf, bytes, ws, sms);
         run_guided<Red<IPM_MUL, IPM_I64>>("i64*", buf, bytes, ws, sms);
         run_guided<Red<IPM_MAX, IPM_F64>>("f64max", buf, bytes, ws, sms);
+      }
+    }
+  }
+  if (mode == "tmaflat") {
+    for (int i = 0; i < 30; ++i) k_flat<Red<IPM_ADD, IPM_F32>, 256, 4, 0, 0><<<sms * 4, 256>>>(FlatParams{buf, (int64_t)(big / 4), 0, 0, 0, MODE_PARTIAL, (char*)ws + 4160, (uint64_t*)((char*)ws + 8192), (unsigned*)ws, nullptr, 0});
+    CK(cudaDeviceSynchronize());
+    for (size_t bytes : {(size_t)1 << 30, (size_t)16 << 30}) {
+      printf("== tmaflat %zu GiB\n", bytes >> 30);
+      for (int rep = 0; rep < 2; ++rep) {
+        run_flat<Red<IPM_ADD, IPM_F32>, 256, 4, 0, 0>("f32+", buf, bytes, ws, sms, 4);
+        run_guided<Red<IPM_ADD, IPM_F32>>("f32+", buf, bytes, ws, sms);
+#define TMAV(RED, NAME)                                                           \
+        run_flat_tma<RED, 8, 16384, 256, 1, 0>(NAME, buf, bytes, ws, sms);            \
+        run_flat_tma<RED, 8, 16384, 256, 1, 1>(NAME, buf, bytes, ws, sms);            \
+        run_flat_tma<RED, 8, 16384, 256, 1, 2>(NAME, buf, bytes, ws, sms);            \
+        run_flat_tma<RED, 12, 16384, 256, 1, 1>(NAME, buf, bytes, ws, sms);           \
+        run_flat_tma<RED, 6, 32768, 256, 1, 1>(NAME, buf, bytes, ws, sms);
+        using Rf32 = Red<IPM_ADD, IPM_F32>;
+        using Rf64 = Red<IPM_ADD, IPM_F64>;
+        using Ri32 = Red<IPM_BXOR, IPM_I32>;
+        using Rmax = Red<IPM_MAX, IPM_F64>;
+        TMAV(Rf32, "f32+")
+        TMAV(Rf64, "f64+")
+        TMAV(Ri32, "i32^")
+        TMAV(Rmax, "f64max")
+        run_flat<Red<IPM_BXOR, IPM_I32>, 256, 4, 0, 0>("i32^", buf, bytes, ws, sms, 4);
       }
     }
   }
