@@ -442,7 +442,7 @@ def run_ours(args, rank, world, local_rank):
             "elements_per_s": N_TOTAL / (ms_step / 1e3),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "k_flat_guided<Red<+,f32>,256,4> (one launch per step per GPU)",
+                         "kernel": "k_flat_guided<Red<+,f32>,256,2,pipelined> (one launch per step per GPU)",
                          "bytes_per_launch": n_shard * ELEM, "kernel_ms_avg": kern_avg,
                          "kernel_ms_min": min(kern_ms), "launches_timed": len(kern_ms),
                          "vs_8TBs_spec": achieved / 8000.0},

@@ -50,7 +50,8 @@ static int env_int(const char* name, int dflt) {
 
 // tuning (compile-time kernel shapes, run-time grid sizing)
 constexpr int FLAT_BLOCK = 256;
-constexpr int FLAT_U = 4;  // 4 x 32 B in flight per thread
+constexpr int FLAT_U = 4;    // static / dynamic k_flat: 4 x 32 B loads per thread per tile
+constexpr int GUIDED_U = 2;  // k_flat_guided: 2 x 32 B per tile, software-pipelined (2-4 loads in flight)
 // run-time options (ipm_set_option); defaults chosen by tools/sweep_flat.cu measurements
 static int g_opt_flat_cps = -1;  // CTAs per SM for k_flat (-1: IPM_CTAS_PER_SM env or 4)
 static int g_opt_seg_kernel = 0; // 0 auto, 1 k_seg_warp (LDG), 2 k_seg_tma (bulk copies)
@@ -164,7 +165,7 @@ struct Launch {
   // mode keep the static grid-stride schedule.
   static void flat(const FlatParams& p, dim3 grid, cudaStream_t st) {
     if (p.counter && grid.y == 1 && grid.x > 1 && g_opt_deterministic != 2) {
-      if (g_opt_deterministic) k_flat_guided<R, FLAT_BLOCK, FLAT_U><<<grid, FLAT_BLOCK, 0, st>>>(p);
+      if (g_opt_deterministic) k_flat_guided<R, FLAT_BLOCK, GUIDED_U, true><<<grid, FLAT_BLOCK, 0, st>>>(p);
       else k_flat<R, FLAT_BLOCK, FLAT_U, 0, 2><<<grid, FLAT_BLOCK, 0, st>>>(p);
     } else {
       k_flat<R, FLAT_BLOCK, FLAT_U, 0, 0><<<grid, FLAT_BLOCK, 0, st>>>(p);

@@ -280,6 +280,27 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_flat(FlatParams p) {
   };
   if (SCHED == 0) {
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) tile(t);
+  } else if (SCHED == 3) {  // static grid-stride, software-pipelined: the next tile's loads are issued first
+    int64_t t = blockIdx.x;
+    VT nx[U];
+    if (t < ntiles) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) nx[u] = ldv<HINT>(vp + t * TILE + threadIdx.x + u * BLOCK);
+    }
+    for (; t < ntiles; t += gridDim.x) {
+      VT cu[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) cu[u] = nx[u];
+      const int64_t tn = t + gridDim.x;
+      if (tn < ntiles) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) nx[u] = ldv<HINT>(vp + tn * TILE + threadIdx.x + u * BLOCK);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int k = 0; k < VW; ++k) acc[k] = R::op(acc[k], R::lift(cu[u].w[k]));
+    }
   } else if (SCHED == 1) {
     const int64_t t1 = (ntiles * (blockIdx.x + 1)) / gridDim.x;
     for (int64_t t = (ntiles * blockIdx.x) / gridDim.x; t < t1; ++t) tile(t);
@@ -325,7 +346,7 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_flat(FlatParams p) {
 // head and tail scalars). Every slot's value depends only on its element range and the fixed thread mapping —
 // not on which CTA computed it — and the last CTA folds the G + K + 1 slots in slot order, so the result is
 // bit-identical run to run while fast SMs absorb the slow ones' share of the tail.
-template <class R, int BLOCK, int U>
+template <class R, int BLOCK, int U, bool PIPE = false>
 __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_flat_guided(FlatParams p) {
   using B = typename R::B;
   using A = typename R::A;
@@ -387,8 +408,32 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_flat_guided(FlatParams 
   };
 
   // static part
+  // fold tiles first, first + stride, ... (count of them) with the next tile's loads issued before the
+  // current tile is folded (software pipelining: loads stay in flight while the previous tile is consumed)
+  auto run = [&](int64_t first, int64_t stride, int64_t count) {
+    if (count <= 0) return;
+    VT nx[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) nx[u] = ldv(vp + first * TILE + threadIdx.x + u * BLOCK);
+    for (int64_t k = 0; k < count; ++k) {
+      VT cu[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) cu[u] = nx[u];
+      if (k + 1 < count) {
+        const int64_t tn = first + (k + 1) * stride;
+#pragma unroll
+        for (int u = 0; u < U; ++u) nx[u] = ldv(vp + tn * TILE + threadIdx.x + u * BLOCK);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int kk = 0; kk < VW; ++kk) acc[kk] = R::op(acc[kk], R::lift(cu[u].w[kk]));
+    }
+  };
   reset();
-  for (int64_t k = 0; k < srounds; ++k) tile(blockIdx.x + k * G);
+  if (PIPE) run(blockIdx.x, G, srounds);
+  else
+    for (int64_t k = 0; k < srounds; ++k) tile(blockIdx.x + k * G);
   if (threadIdx.x == 0) s_c = (long long)atomicAdd(p.counter, 1ull);  // claim the first dynamic chunk
   publish(blockIdx.x);
   long long c = s_c;
@@ -400,7 +445,10 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_flat_guided(FlatParams 
     if (c < K) {
       const int64_t e1 = dyn0 + (int64_t)(c + 1) * ct;
       const int64_t t1 = e1 < ntiles ? e1 : ntiles;
-      for (int64_t t = dyn0 + (int64_t)c * ct; t < t1; ++t) tile(t);
+      const int64_t t0 = dyn0 + (int64_t)c * ct;
+      if (PIPE) run(t0, 1, t1 - t0);
+      else
+        for (int64_t t = t0; t < t1; ++t) tile(t);
     } else {
       for (int64_t i = ntiles * TILE + threadIdx.x; i < nv; i += BLOCK) {
         const VT v = ldv(vp + i);

@@ -32,3 +32,25 @@ h = np.arange(100_000, dtype=np.int64)
 ipm.reduce_host("+", h)
 torch.cuda.synchronize()
 print("sanitize_run: ok")
+# ragged rows, several variables, 2-D region, the fused multi-rank exchange (2 ranks, one GPU)
+for dt in TD:
+    off = np.array([0, 3, 3, 40, 41, 300, 300, 5000], np.int64) + 2
+    x = torch.empty(int(off[-1]) + 3, dtype=TD[dt], device="cuda")
+    ipmgen.fill_device(ipmgen.Spec(dt, x.numel(), "random", seed=2), x.data_ptr(), 0, x.numel(),
+                       torch.cuda.current_stream().cuda_stream)
+    ipm.reduce_ragged("+", x, torch.from_numpy(off).cuda())
+    for sig in ("sum_sumsq", "dot", "minmax", "stats"):
+        ipm.reduce_fused(sig, x[1:2001], x[3:2003] if sig == "dot" else None)
+    ipm.reduce_2d("max", x, rows=7, cols=300, row_stride=700)
+ipm.set_option("dist_timeout_ms", 3000)  # the sanitizer may serialise the two ranks' kernels
+comms = ipm.Comm.group(2)
+y = torch.arange(100_003, dtype=torch.float64, device="cuda")
+ss = [torch.cuda.Stream() for _ in range(2)]
+wss = [torch.zeros(ipm.WS_BYTES, dtype=torch.uint8, device="cuda") for _ in range(2)]
+for r, c in enumerate(comms):
+    lo, hi = ipm.shard_range(y.numel(), r, 2)
+    c.reduce_async("+", y[lo:hi], ws=wss[r], stream=ss[r])
+torch.cuda.synchronize()
+for c in comms:
+    c.close()
+print("sanitize_run (extended): ok")
