@@ -370,7 +370,10 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_flat_guided(FlatParams 
   const int64_t dyn0 = srounds * G;
   const int64_t rem = ntiles - dyn0;
   const int64_t max_chunks = p.max_chunks > 0 ? p.max_chunks : 1;
-  const int64_t ct = rem > 0 ? (rem + max_chunks - 1) / max_chunks : 1;
+  // tiles per dynamic chunk: enough chunks to balance, >= 4 tiles each to amortise the per-chunk block
+  // reduction (tools/sweep_flat.cu "chunks": 1-tile chunks cost 2.6% at 1 GiB)
+  int64_t ct = rem > 0 ? (rem + max_chunks - 1) / max_chunks : 1;
+  if (ct < 4) ct = 4;
   const int64_t K = (rem + ct - 1) / ct;                 // dynamic chunks 0..K-1; chunk K = the remainder
   uint64_t* slots = p.partials;
 
