@@ -336,7 +336,7 @@ def run_ours(args, rank, world, local_rank):
 
     # clock spin-up (setup, untimed): ~0.25 s of back-to-back steps so the timed steps run at steady clocks.
     # The count is a function of the shard size only, identical on every rank (every call is collective).
-    spin = max(3, int(0.25 / (n_shard * ELEM / 7.0e12)))
+    spin = max(3, int(0.25 / (N_TOTAL / world * ELEM / 7.0e12)))
     spin = min(spin, 2000)
     for _ in range(spin):
         comm.reduce_async("+", x, init=init, out=out, ws=ws)
