@@ -188,7 +188,7 @@ ipm_status ipm_reduce_fused_async(ipm_fused f, ipm_dtype dt, const void* x, cons
  * undefined otherwise). dev: the element array (indices off[0] .. off[rows]-1 are read). dev_out: rows
  * elements. Work is balanced by elements, not rows: rows of any length, including a few huge ones, spread over
  * all SMs; rows split between warps are finished by a second one-warp-per-split kernel, folding the pieces in
- * order (deterministic). Two kernel launches; workspace required. */
+ * order (deterministic). Two kernel launches; workspace required. rows < 2^31 - 1 (else IPM_E_SIZE). */
 ipm_status ipm_reduce_ragged(ipm_op op, ipm_dtype dt, const void* dev, const int64_t* dev_offsets, int64_t rows,
                              const void* init, void* dev_out, void* workspace, void* stream);
 

@@ -687,6 +687,10 @@ ipm_status ipm_reduce_ragged(ipm_op op, ipm_dtype dt, const void* dev, const int
     return IPM_E_SIZE;
   }
   if (rows == 0) return IPM_OK;
+  if (rows >= INT32_MAX) {
+    set_error("ragged: at most 2^31-2 rows");
+    return IPM_E_SIZE;
+  }
   if (!dev_offsets || !dev_out) {
     set_error("NULL device pointer");
     return IPM_E_NULL;

@@ -847,10 +847,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_vec(RaggedParams p)
   constexpr int EPL = VW * VPL;  // elements per lane per chunk (<= 32: one flag bit each)
   constexpr int CH = 32 * EPL;   // elements per chunk
   static_assert(EPL <= 32, "flag word");
-  __shared__ long long s_rid[WARPS][CH];  // chunk position -> row starting there (valid where flagged)
+  __shared__ int s_rid[WARPS][CH];        // chunk position -> (row - r0) starting there (valid where flagged)
   __shared__ unsigned s_flag[WARPS][32];  // per lane: bit k = a row starts at the lane's element k
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  long long* rid_map = s_rid[wid];
+  int* rid_map = s_rid[wid];
   unsigned* flagw = s_flag[wid];
   flagw[lane] = 0u;
   const unsigned lanemask_lt = (1u << lane) - 1u;
@@ -888,33 +888,39 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_vec(RaggedParams p)
     // chunk bases: positions whose address is 32-byte aligned
     const int64_t q0 = lo - (int64_t)(((uintptr_t)(a + lo) & 31u) / sizeof(B));
     for (int64_t Bc = q0; Bc < hi; Bc += CH) {
+      // valid positions of this chunk, relative to Bc: [rlo_c, rhi_c)
+      const int rlo_c = (int)(lo > Bc ? lo - Bc : 0);
+      const int rhi_c = (int)(hi - Bc < CH ? hi - Bc : CH);
+      const bool interior = rlo_c == 0 && rhi_c == CH;  // warp-uniform
       // this lane's elements, issued first: positions Bc + EPL*lane + k
-      const int64_t p0 = Bc + (int64_t)EPL * lane;
+      const B* pl = a + Bc + EPL * lane;
       B x[EPL];
+      if (interior) {
 #pragma unroll
-      for (int v = 0; v < VPL; ++v) {
-        const int64_t pv = p0 + v * VW;
-        if (pv >= lo && pv + VW <= hi) {
-          const VT t = ldv((const VT*)(a + pv));
+        for (int v = 0; v < VPL; ++v) {
+          const VT t = ldv((const VT*)(pl + v * VW));
 #pragma unroll
           for (int k = 0; k < VW; ++k) x[v * VW + k] = t.w[k];
-        } else {
+        }
+      } else {
 #pragma unroll
-          for (int k = 0; k < VW; ++k) x[v * VW + k] = (pv + k >= lo && pv + k < hi) ? lds(a + pv + k) : (B)0;
+        for (int k = 0; k < EPL; ++k) {
+          const int rel = EPL * lane + k;
+          x[k] = (rel >= rlo_c && rel < rhi_c) ? lds(pl + k) : (B)0;
         }
       }
-      const int64_t cl = Bc > lo ? Bc : lo, ch = Bc + CH < hi ? Bc + CH : hi;  // valid positions [cl, ch)
-      // rows starting in [cl, ch): flag their start position; empty ones are finished here
+      // rows starting in the chunk's valid range: flag their start position; empty ones are finished here
       while (true) {
         const int64_t r = wb + lane;
-        const bool inr = r < p.rows && sw >= cl && sw < ch;
+        const int64_t d = sw - Bc;
+        const bool inr = r < p.rows && d >= rlo_c && d < rhi_c;
         if (inr && ew > sw) {
-          const int rel = (int)(sw - Bc);
-          rid_map[rel] = r;
+          const int rel = (int)d;
+          rid_map[rel] = (int)(r - r0);
           atomicOr(&flagw[rel / EPL], 1u << (rel % EPL));
         }
         if (inr && ew == sw) finish(r, R::id());
-        const bool done = r >= p.rows || sw < ch;
+        const bool done = r >= p.rows || d < rhi_c;
         if (__all_sync(FULL, done) && wb + 32 < p.rows) {
           wb += 32;
           load_window(wb, sw, ew);
@@ -925,26 +931,44 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_vec(RaggedParams p)
       __syncwarp();
       const unsigned fl = flagw[lane];
       flagw[lane] = 0u;
-      const int rlo = (int)(lo > p0 ? (lo - p0 < EPL ? lo - p0 : EPL) : 0);  // valid k in [rlo, rhi)
-      const int rhi = (int)(hi > p0 ? (hi - p0 < EPL ? hi - p0 : EPL) : 0);
-      // lane-local fold with row breaks: head = before the first flag, tail = from the last flag
+      // lane-local fold: head = elements before the first flag, tail = from the last flag on; rows that start
+      // and end inside this lane (two or more flags) are finished separately
+      A xv[EPL];
+      if (interior) {
+#pragma unroll
+        for (int k = 0; k < EPL; ++k) xv[k] = R::lift(x[k]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < EPL; ++k) {
+          const int rel = EPL * lane + k;
+          xv[k] = (rel >= rlo_c && rel < rhi_c) ? R::lift(x[k]) : R::id();
+        }
+      }
+      const int kf = fl ? __ffs(fl) - 1 : EPL;
+      const int kl = fl ? 31 - __clz(fl) : EPL;
       A head = R::id(), cur = R::id();
-      int lastk = -1;
 #pragma unroll
       for (int k = 0; k < EPL; ++k) {
-        const A xv = (k >= rlo && k < rhi) ? R::lift(x[k]) : R::id();
-        if ((fl >> k) & 1u) {
-          if (lastk >= 0) finish(rid_map[EPL * lane + lastk], cur);  // a whole row inside this lane
-          else head = cur;
-          cur = xv;
-          lastk = k;
-        } else {
-          cur = R::op(cur, xv);
+        if (k < kf) head = R::op(head, xv[k]);
+        if (k >= kl) cur = R::op(cur, xv[k]);
+      }
+      if (__popc(fl) >= 2) {  // whole rows inside this lane
+        unsigned m = fl & ~(1u << kl);
+        while (m) {
+          const int k0 = __ffs(m) - 1;
+          m &= m - 1;
+          const unsigned rest = fl & ~((2u << k0) - 1u);
+          const int k1 = __ffs(rest) - 1;
+          A v = R::id();
+#pragma unroll
+          for (int k = 0; k < EPL; ++k)
+            if (k >= k0 && k < k1) v = R::op(v, xv[k]);
+          finish(r0 + rid_map[EPL * lane + k0], v);
         }
       }
       const bool flag = fl != 0u;
-      if (!flag) head = cur;
-      const long long my_rid = flag ? rid_map[EPL * lane + lastk] : -1;
+      const int lastk = kl;
+      const long long my_rid = flag ? (long long)(r0 + rid_map[EPL * lane + lastk]) : -1;
       // segmented inclusive scan over lanes: a flagged lane starts a segment with its tail value
       const unsigned bal = __ballot_sync(FULL, flag);
       const unsigned le = bal & (lanemask_lt | (1u << lane));
