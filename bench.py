@@ -239,6 +239,30 @@ def suite(ipm, torch, ipmgen, peak):
             gbs = x.numel() * x.element_size() / med / 1e6
             out[f"C4_{dt}_{op}_2^30"] = {"kernel_ms_median": med, "GB/s": gbs, "frac": gbs / peak}
         del x
+    # library context (not targets): torch's own reductions on the same shapes, CUDA events on torch's stream
+    def torch_timed(fn, reps=20):
+        t0 = time.perf_counter()
+        while time.perf_counter() - t0 < 0.1:
+            fn()
+            torch.cuda.synchronize()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+        for a, b in evs:
+            a.record()
+            fn()
+            b.record()
+        torch.cuda.synchronize()
+        return statistics.median([a.elapsed_time(b) for a, b in evs])
+    ctx = {}
+    for dt, tdt, n in (("float32", torch.float32, 1 << 28), ("float64", torch.float64, 1 << 28),
+                       ("int32", torch.int32, 1 << 30)):
+        x = torch.empty(n, dtype=tdt, device="cuda")
+        ipmgen.fill_tensor(ipmgen.Spec(dt, n, "random", seed=1), x)
+        for name, fn in (("torch.sum", lambda: x.sum()), ("torch.amax", lambda: x.amax())):
+            ms = torch_timed(fn)
+            ctx[f"{name}_{dt}_2^{n.bit_length() - 1}"] = {"ms": ms, "GB/s": n * x.element_size() / ms / 1e6}
+        del x
+    out["library_context_torch"] = ctx
+
     # NEXT rows: several variables in one pass (SRAD statistics, dot) and a strided 2-D region
     n = 1 << 28
     x = torch.empty(n, dtype=torch.float32, device="cuda")

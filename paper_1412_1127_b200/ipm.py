@@ -380,12 +380,12 @@ def identity_value(op: str, dt: int):
 
 OPTIONS = {"flat_ctas_per_sm": 0, "seg_kernel": 1, "deterministic": 2, "dist_mode": 3, "dist_timeout_ms": 4}
 DIST_MODES = {"auto": 0, "p2p": 0, "nccl": 1}
-SEG_KERNELS = {"auto": 0, "ldg": 1, "tma": 2}
+SEG_KERNELS = {"auto": 0, "warp": 1, "ldg": 1, "tma": 2}
 
 
 def set_option(key: str, value) -> None:
     """Process-wide tuning option (ipm_set_option): flat_ctas_per_sm (1..8, -1 default), seg_kernel
-    ('auto' | 'ldg' | 'tma')."""
+    ('auto' | 'warp' | 'tma')."""
     if key == "seg_kernel" and isinstance(value, str):
         value = SEG_KERNELS[value]
     if key == "dist_mode" and isinstance(value, str):

@@ -54,3 +54,10 @@ torch.cuda.synchronize()
 for c in comms:
     c.close()
 print("sanitize_run (extended): ok")
+for dt in TD:  # one CTA per row (long rows, many of them)
+    x = torch.empty(600 * 1100 + 5, dtype=TD[dt], device="cuda")
+    ipmgen.fill_device(ipmgen.Spec(dt, x.numel(), "random", seed=3), x.data_ptr(), 0, x.numel(),
+                       torch.cuda.current_stream().cuda_stream)
+    ipm.reduce_segmented("+", x[1:], rows=600, cols=1100, row_stride=1100)
+torch.cuda.synchronize()
+print("sanitize_run (seg cta): ok")
