@@ -213,9 +213,10 @@ ipm_status ipm_profile_disable(void);
 
 /* Tuning options (process-wide; the defaults are the measured best):
  *   IPM_OPT_FLAT_CTAS_PER_SM  CTAs per SM of the flat kernel's persistent grid, 1..8 (-1 = default 4)
- *   IPM_OPT_SEG_KERNEL        segmented rows: 0 auto (one CTA per row for >= 4 KiB rows when rows >= 4 x SMs,
- *                             else one warp per row; direct 256-bit loads), 1 one warp per row, 2 TMA bulk
- *                             copies into a per-warp shared-memory ring (rows of >= 64 bytes)
+ *   IPM_OPT_SEG_KERNEL        segmented rows: 0 auto (= 1), 1 one warp per row with direct 256-bit loads,
+ *                             2 one warp per row fed by TMA bulk copies into a per-warp shared-memory ring
+ *                             (rows of >= 64 bytes). (One CTA per row was measured slower: profiles/
+ *                             r01_seg_kernels.txt.)
  *   IPM_OPT_DETERMINISTIC     1 (default): the flat clause uses the guided schedule — ~90% of the tiles
  *                             dealt statically, the rest in fixed chunks claimed dynamically, one partial per
  *                             element range, folded in a fixed order — so repeated runs give identical bits

@@ -54,7 +54,7 @@ constexpr int FLAT_U = 4;    // static / dynamic k_flat: 4 x 32 B loads per thre
 constexpr int GUIDED_U = 2;  // k_flat_guided: 2 x 32 B per tile, software-pipelined (2-4 loads in flight)
 // run-time options (ipm_set_option); defaults chosen by tools/sweep_flat.cu measurements
 static int g_opt_flat_cps = -1;  // CTAs per SM for k_flat (-1: IPM_CTAS_PER_SM env or 4)
-static int g_opt_seg_kernel = 0; // 0 auto (CTA per row for long rows, else warp per row), 1 warp per row, 2 TMA
+static int g_opt_seg_kernel = 0; // 0 auto (= 1), 1 warp per row (direct loads), 2 warp per row (TMA ring)
 static int g_opt_deterministic = 1;  // 1: guided deterministic schedule for the flat kernel
 static int g_opt_dist_mode = 0;      // 0: fused peer-memory exchange when mapped, 1: NCCL AllGather
 static long long g_opt_dist_timeout_ms = 30000;
@@ -174,9 +174,6 @@ struct Launch {
   static void seg_warp(const SegParams& p, int grid, cudaStream_t st) {
     k_seg_warp<R, SEG_WARPS, SEG_U><<<grid, SEG_WARPS * 32, 0, st>>>(p);
   }
-  static void seg_cta(const SegParams& p, int grid, cudaStream_t st) {
-    k_seg_cta<R, FLAT_BLOCK, 2><<<grid, FLAT_BLOCK, 0, st>>>(p);
-  }
   static void ragged(const RaggedParams& p, int blocks, int64_t nw, cudaStream_t st) {
     k_ragged_vec<R, 8, 4, 2><<<blocks, 256, 0, st>>>(p);  // 4 CTAs x 8 warps per SM, 2 vectors per lane
     k_ragged_fix<R><<<(unsigned)((nw + 7) / 8), 256, 0, st>>>(p, nw);
@@ -210,7 +207,6 @@ struct Table {
   void (*flat)(const FlatParams&, dim3, cudaStream_t);
   void (*two_d)(const Params2D&, int, cudaStream_t);
   void (*ragged)(const RaggedParams&, int, int64_t, cudaStream_t);
-  void (*seg_cta)(const SegParams&, int, cudaStream_t);
   void (*seg_warp)(const SegParams&, int, cudaStream_t);
   cudaError_t (*seg_tma)(const SegParams&, int, cudaStream_t);
   void (*seg_group)(const SegParams&, int, int, cudaStream_t);
@@ -220,7 +216,7 @@ struct Table {
 static const Table* table(ipm_op op, ipm_dtype dt) {
 #define IPM_ENTRY(O, D)                                                                                  \
   if (op == O && dt == D) {                                                                            \
-    static const Table t = {&Launch<O, D>::flat, &Launch<O, D>::two_d, &Launch<O, D>::ragged, &Launch<O, D>::seg_cta, &Launch<O, D>::seg_warp, &Launch<O, D>::seg_tma,     \
+    static const Table t = {&Launch<O, D>::flat, &Launch<O, D>::two_d, &Launch<O, D>::ragged, &Launch<O, D>::seg_warp, &Launch<O, D>::seg_tma,     \
                             &Launch<O, D>::seg_group, &Launch<O, D>::finalize};                        \
     return &t;                                                                                         \
   }
@@ -611,10 +607,6 @@ ipm_status ipm_reduce_segmented(ipm_op op, ipm_dtype dt, const void* dev, int64_
   if (tma) {         // one warp per row, rows staged by TMA bulk copies (one 128 KiB-ring CTA per SM)
     const int64_t blocks = std::min<int64_t>((rows + TMA_WARPS - 1) / TMA_WARPS, (int64_t)sms);
     CK(t->seg_tma(p, (int)std::max<int64_t>(1, blocks), st));
-  } else if (g_opt_seg_kernel != 1 && cols * (int64_t)esize(dt) >= 4096 && rows >= 4 * (int64_t)sms) {
-    // long rows, many of them: one CTA per row (short grid tail)
-    const int64_t blocks = std::min<int64_t>(rows, (int64_t)sms * flat_ctas_per_sm());
-    t->seg_cta(p, (int)blocks, st);
   } else if (cols >= 32) {  // one warp per row, direct 256-bit loads
     const int64_t blocks = std::min<int64_t>((rows + SEG_WARPS - 1) / SEG_WARPS, (int64_t)sms * 4);
     t->seg_warp(p, (int)std::max<int64_t>(1, blocks), st);

@@ -735,82 +735,6 @@ __global__ void __launch_bounds__(WARPS * 32) k_seg_tma(SegParams p) {
   }
 }
 
-// long rows: one CTA per row (grid-stride over rows). Each row is split over all BLOCK threads, so one row
-// costs a CTA ~1 us instead of a warp ~10 us and the grid's tail is short; the next row's first tile is loaded
-// before the current row is reduced (software pipelining across rows).
-template <class R, int BLOCK, int U>
-__global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_seg_cta(SegParams p) {
-  using B = typename R::B;
-  using A = typename R::A;
-  using VT = typename Vec<B>::T;
-  constexpr int VW = Vec<B>::W;
-  constexpr int64_t TILE = (int64_t)BLOCK * U;
-  __shared__ A sm[BLOCK / 32];
-  struct Geo {
-    const B* a;
-    int64_t head, nv, tail0;
-    const VT* vp;
-  };
-  auto geo = [&](int64_t r) {
-    Geo g;
-    g.a = (const B*)p.a + r * p.row_stride;
-    g.head = (int64_t)(((32u - ((uintptr_t)g.a & 31u)) & 31u) / sizeof(B));
-    if (g.head > p.cols) g.head = p.cols;
-    g.nv = (p.cols - g.head) / VW;
-    g.tail0 = g.head + g.nv * VW;
-    g.vp = (const VT*)(g.a + g.head);
-    return g;
-  };
-  auto load_tile0 = [&](const Geo& g, VT* v) {
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t i = threadIdx.x + (int64_t)u * BLOCK;
-      if (i < g.nv) v[u] = ldv(g.vp + i);
-    }
-  };
-  int64_t r = blockIdx.x;
-  if (r >= p.rows) return;
-  Geo g = geo(r);
-  VT nx[U];
-  load_tile0(g, nx);
-  for (; r < p.rows; r += gridDim.x) {
-    A acc[VW];
-#pragma unroll
-    for (int k = 0; k < VW; ++k) acc[k] = R::id();
-    VT cu[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) cu[u] = nx[u];
-    const Geo gc = g;
-    const int64_t rn = r + gridDim.x;
-    if (rn < p.rows) {
-      g = geo(rn);
-      load_tile0(g, nx);
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (threadIdx.x + (int64_t)u * BLOCK < gc.nv)
-#pragma unroll
-        for (int k = 0; k < VW; ++k) acc[k] = R::op(acc[k], R::lift(cu[u].w[k]));
-    for (int64_t i = TILE + threadIdx.x; i < gc.nv; i += BLOCK) {  // rows longer than one tile
-      const VT v = ldv(gc.vp + i);
-#pragma unroll
-      for (int k = 0; k < VW; ++k) acc[k] = R::op(acc[k], R::lift(v.w[k]));
-    }
-    if (threadIdx.x < gc.head) acc[0] = R::op(acc[0], R::lift(lds(gc.a + threadIdx.x)));
-    if (threadIdx.x < p.cols - gc.tail0) acc[VW - 1] = R::op(acc[VW - 1], R::lift(lds(gc.a + gc.tail0 + threadIdx.x)));
-#pragma unroll
-    for (int s2 = VW / 2; s2 > 0; s2 >>= 1)
-#pragma unroll
-      for (int k = 0; k < s2; ++k) acc[k] = R::op(acc[k], acc[k + s2]);
-    A t = block_reduce<R, BLOCK>(acc[0], sm);
-    if (threadIdx.x == 0) {
-      if (p.has_init) t = R::op(R::lift((B)p.init), t);
-      ((B*)p.out)[r] = R::fin(t);
-    }
-    __syncthreads();  // sm reuse
-  }
-}
-
 // short rows: G lanes per row (G in 1,2,4,8,16), 32/G rows per warp step; scalar loads (coalesced across
 // the warp when rows are contiguous)
 template <class R, int G>
