@@ -158,6 +158,16 @@ def _stream(stream=None) -> int:
     return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
 
 
+def _sync(stream=None) -> None:
+    """Wait for `stream` (None = torch's current stream) before reading results on the host."""
+    if stream is None:
+        torch.cuda.current_stream().synchronize()
+    elif hasattr(stream, "synchronize"):
+        stream.synchronize()
+    else:
+        torch.cuda.ExternalStream(int(stream)).synchronize()
+
+
 def _scalar(dt: int, value):
     """a 1-element numpy buffer holding `value` in element type dt (None -> None)"""
     if value is None:
@@ -199,7 +209,9 @@ def reduce(op: str, t: torch.Tensor, init=None, ws: torch.Tensor | None = None, 
     ws = workspace(stream) if ws is None else ws
     box = _scalar(dt, init)
     if box is None:  # no original value: start from the identity (the async path does that on device)
-        return reduce_async(op, t, None, ws=ws, stream=stream).cpu().numpy()[0]
+        out = reduce_async(op, t, None, ws=ws, stream=stream)
+        _sync(stream)
+        return out.cpu().numpy()[0]
     _check(lib.ipm_reduce(op_code(op), dt, ptr, n, box.ctypes.data, ws.data_ptr(), s), "ipm_reduce")
     return box[0]
 
@@ -308,6 +320,7 @@ def reduce_2d(op: str, t: torch.Tensor, rows: int | None = None, cols: int | Non
     _check(lib.ipm_reduce_2d_async(op_code(op), dt, t.data_ptr(), rows, cols, row_stride,
                                    None if box is None else box.ctypes.data, out.data_ptr(), ws.data_ptr(),
                                    _stream(stream)), "ipm_reduce_2d_async")
+    _sync(stream)
     return out.cpu().numpy()[0]
 
 
@@ -339,7 +352,9 @@ def reduce_fused(sig: str, x: torch.Tensor, y: torch.Tensor | None = None, init=
                  ws: torch.Tensor | None = None, stream=None) -> np.ndarray:
     """Blocking form: returns the variables as a numpy array (init: one value per variable, or None)."""
     if init is None:
-        return reduce_fused_async(sig, x, y, None, ws=ws, stream=stream).cpu().numpy()
+        out = reduce_fused_async(sig, x, y, None, ws=ws, stream=stream)
+        _sync(stream)
+        return out.cpu().numpy()
     f = FUSED[sig]
     ptr, n, dt = _flat_arg(x)
     yp = _flat_arg(y)[0] if f == FUSED["dot"] else None
@@ -560,6 +575,7 @@ class Comm:
         box = _scalar(dt, init)
         if box is None:
             out = self.reduce_async(op, shard, None, ws=ws, stream=stream)
+            _sync(stream)
             return out.cpu().numpy()[0]
         _check(lib.ipm_reduce_dist(self._h, op_code(op), dt, ptr, n, box.ctypes.data, ws.data_ptr(),
                                    _stream(stream)), "ipm_reduce_dist")
