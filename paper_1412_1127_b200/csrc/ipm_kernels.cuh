@@ -872,15 +872,22 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_vec(RaggedParams p)
     if (p.has_init) v = R::op(R::lift((B)p.init), v);
     ((B*)p.out)[row] = R::fin(v);
   };
-  // window of row offsets: lane l holds off[wb + l] and off[wb + l + 1]
+  // window of row offsets: lane l holds off[wb + l] and off[wb + l + 1]; the offsets are loaded two windows
+  // ahead (one coalesced load per lane per window; the end offsets come from the neighbour lane)
   int64_t wb = r0;
-  auto load_window = [&](int64_t base, int64_t& s0, int64_t& e0) {
+  auto fetch = [&](int64_t base) -> int64_t {
     const int64_t r = base + lane;
-    s0 = r <= p.rows ? __ldg(p.off + r) : P1;
-    e0 = r + 1 <= p.rows ? __ldg(p.off + r + 1) : P1;
+    return r <= p.rows ? __ldg(p.off + r) : P1;
   };
-  int64_t sw, ew;
-  load_window(wb, sw, ew);
+  auto ends = [&](int64_t s0, int64_t nxt0) -> int64_t {  // off[wb + lane + 1]
+    const int64_t up = __shfl_down_sync(FULL, s0, 1);
+    const int64_t n0 = __shfl_sync(FULL, nxt0, 0);
+    return lane == 31 ? n0 : up;
+  };
+  int64_t sw = fetch(wb);
+  int64_t nx = fetch(wb + 32);   // the next window
+  int64_t nx2 = fetch(wb + 64);  // and the one after (its first offset closes the next window's last row)
+  int64_t ew = ends(sw, nx);
   int64_t open_rid = hrow;
   A open_val = R::id();
   __syncwarp();
@@ -923,7 +930,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_vec(RaggedParams p)
         const bool done = r >= p.rows || d < rhi_c;
         if (__all_sync(FULL, done) && wb + 32 < p.rows) {
           wb += 32;
-          load_window(wb, sw, ew);
+          sw = nx;
+          nx = nx2;
+          nx2 = fetch(wb + 64);
+          ew = ends(sw, nx);
           continue;
         }
         break;
