@@ -474,3 +474,43 @@ def test_dist_fused_multirank_one_gpu(ipm, world):
             check(op, dt, vals[0], want_t, want_ld)
     for c in comms:
         c.close()
+
+
+# --------------------------------------------------------------------------- options, data clauses, host path edges
+
+@pytest.mark.parametrize("cps", [1, 2, 8])
+@pytest.mark.parametrize("det", [0, 1, 2])
+def test_flat_options_keep_results(ipm, cps, det):
+    ipm.set_option("flat_ctas_per_sm", cps)
+    ipm.set_option("deterministic", det)
+    try:
+        for op, dt, n in [("+", "float64", 5_000_011), ("^", "int32", 3_000_001), ("max", "float32", 777_777)]:
+            spec = workload(op, dt, n, seed=cps * 10 + det)
+            want_t, want_ld = oracle.reduce(op, ipmgen.fill_host(spec), init=NPT[dt](2))
+            check(op, dt, ipm.reduce(op, device_input(spec, offset=1), init=NPT[dt](2)), want_t, want_ld)
+    finally:
+        ipm.set_option("flat_ctas_per_sm", -1)
+        ipm.set_option("deterministic", 1)
+
+
+def test_update_clauses_and_host_edges(ipm):
+    h = np.arange(10_000, dtype=np.int64)
+    d = ipm.copyin(h)
+    t = ipm.as_tensor(d, h.size, torch.int64)
+    assert ipm.reduce("+", t) == h.sum()
+    h[:] = 2                                   # acc update device(h)
+    ipm.update_device(h)
+    assert ipm.reduce("+", t) == 20_000
+    t.fill_(3)                                 # acc update host(h)
+    torch.cuda.synchronize()
+    ipm.update_host(h)
+    assert np.all(h == 3)
+    ipm.copyout(h)
+    assert ipm.present_count() == 0
+    # the fused host path: empty, one element, a size that is not a multiple of the 64 MiB staging chunk
+    assert ipm.reduce_host("+", np.zeros(0, np.float32), init=np.float32(1.5)) == np.float32(1.5)
+    assert ipm.reduce_host("max", np.array([7], np.int32)) == 7
+    big = ipmgen.fill_host(ipmgen.Spec("float32", (1 << 24) * 3 + 17, "random", seed=4))
+    _, want = oracle.reduce("+", big)
+    check("+", "float32", ipm.reduce_host("+", torch.from_numpy(big).pin_memory()), None, want)
+    ipm.lib.ipm_release_staging()

@@ -78,18 +78,18 @@ void run_seg_tma(const char* name, void* buf, void* out, int sms, int64_t rows, 
   }
 }
 
-template <class R, int U = 4, bool PIPE = false>
+template <class R, int U = 4, bool PIPE = false, int BLK = 256>
 void run_guided(const char* name, void* buf, size_t bytes, void* ws, int sms, int64_t maxch = 0) {
   const int64_t n = bytes / sizeof(typename R::B);
   FlatParams p{};
   p.a = buf; p.n = n; p.row_stride = 0; p.init = 0; p.has_init = 0; p.mode = MODE_PARTIAL;
   p.out = (char*)ws + 4160; p.partials = (uint64_t*)((char*)ws + 8192); p.tickets = (unsigned*)ws;
   p.counter = (unsigned long long*)((char*)ws + 4096 + 512);
-  const int grid = sms * 4;
+  const int grid = sms * (1024 / BLK);
   p.max_chunks = maxch ? maxch : 16384 - grid - 1;
-  float ms = time_ms([&] { k_flat_guided<R, 256, U, PIPE><<<grid, 256>>>(p); }, 20);
+  float ms = time_ms([&] { k_flat_guided<R, BLK, U, PIPE><<<grid, BLK>>>(p); }, 20);
   CK(cudaGetLastError());
-  printf("guided %-8s B= 256 U=%d P=%d cps=4 grid=%5d maxch=%6ld  %7.3f ms  %7.1f GB/s\n", name, U, (int)PIPE, grid,
+  printf("guided %-8s B=%4d U=%d P=%d grid=%5d maxch=%6ld  %7.3f ms  %7.1f GB/s\n", name, BLK, U, (int)PIPE, grid,
          (long)p.max_chunks, ms, bytes / ms / 1e6);
 }
 
@@ -271,6 +271,25 @@ int main(int argc, char** argv) {
         run_guided<Red<IPM_MAX, IPM_F32>>("f32max", buf, bytes, ws, sms);
         run_guided<Red<IPM_MUL, IPM_I64>>("i64*", buf, bytes, ws, sms);
         run_guided<Red<IPM_MAX, IPM_F64>>("f64max", buf, bytes, ws, sms);
+      }
+    }
+  }
+  if (mode == "gshape") {
+    for (int i = 0; i < 30; ++i) k_flat<Red<IPM_ADD, IPM_F32>, 256, 4, 0, 0><<<sms * 4, 256>>>(FlatParams{buf, (int64_t)(big / 4), 0, 0, 0, MODE_PARTIAL, (char*)ws + 4160, (uint64_t*)((char*)ws + 8192), (unsigned*)ws, nullptr, 0});
+    CK(cudaDeviceSynchronize());
+    for (size_t bytes : {(size_t)1 << 30, (size_t)16 << 30}) {
+      printf("== gshape %zu GiB\n", bytes >> 30);
+      for (int rep = 0; rep < 2; ++rep) {
+        run_guided<Red<IPM_ADD, IPM_F32>, 2, true, 256>("f32+", buf, bytes, ws, sms);
+        run_guided<Red<IPM_ADD, IPM_F32>, 2, true, 128>("f32+", buf, bytes, ws, sms);
+        run_guided<Red<IPM_ADD, IPM_F32>, 2, true, 512>("f32+", buf, bytes, ws, sms);
+        run_guided<Red<IPM_ADD, IPM_F32>, 1, true, 256>("f32+", buf, bytes, ws, sms);
+        run_guided<Red<IPM_ADD, IPM_F32>, 1, true, 512>("f32+", buf, bytes, ws, sms);
+        run_guided<Red<IPM_ADD, IPM_F32>, 3, true, 256>("f32+", buf, bytes, ws, sms);
+        run_guided<Red<IPM_BXOR, IPM_I32>, 2, true, 256>("i32^", buf, bytes, ws, sms);
+        run_guided<Red<IPM_BXOR, IPM_I32>, 2, true, 128>("i32^", buf, bytes, ws, sms);
+        run_guided<Red<IPM_BXOR, IPM_I32>, 4, true, 128>("i32^", buf, bytes, ws, sms);
+        run_guided<Red<IPM_BXOR, IPM_I32>, 1, true, 512>("i32^", buf, bytes, ws, sms);
       }
     }
   }
