@@ -177,13 +177,11 @@ __global__ void __launch_bounds__(BLOCK) k_fused(FusedParams p) {
     if (S::NV > 1) __stcg(p.partials + gridDim.x + blockIdx.x, pack(c1));
     if (S::NV > 2) __stcg(p.partials + 2 * gridDim.x + blockIdx.x, pack(c2));
     if (S::NV > 3) __stcg(p.partials + 3 * gridDim.x + blockIdx.x, pack(c3));
-    __threadfence();
-    s_last = atomicAdd(p.ticket, 1u) == gridDim.x - 1;
+    s_last = ticket_acq_rel(p.ticket) == gridDim.x - 1;
   }
   __syncthreads();
   const bool last = s_last;
   if (!last) return;
-  __threadfence();
   fused_finish<C0>(p, 0, c0, last, sm8);
   if (S::NV > 1) fused_finish<C1>(p, 1, c1, last, sm8);
   if (S::NV > 2) fused_finish<C2>(p, 2, c2, last, sm8);

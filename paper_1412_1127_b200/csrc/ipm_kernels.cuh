@@ -76,6 +76,14 @@ __device__ __forceinline__ V4 ldv(const V4* p) {
 __device__ __forceinline__ uint32_t lds(const uint32_t* p) { return __ldg(p); }
 __device__ __forceinline__ uint64_t lds(const uint64_t* p) { return (uint64_t)__ldg((const unsigned long long*)p); }
 
+// the cross-CTA ticket: one atomic with release (publishes this CTA's partial, stored before it by the same
+// thread) and acquire (makes every earlier CTA's partial visible; __syncthreads then extends that to the CTA)
+__device__ __forceinline__ unsigned ticket_acq_rel(unsigned* t) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(t) : "memory");
+  return old;
+}
+
 // ------------------------------------------------------------------------------------------ params
 struct FlatParams {
   const void* a;          // row 0 base
@@ -220,13 +228,10 @@ __device__ __forceinline__ void grid_finish(const FlatParams& p, int64_t row, ty
   uint64_t* parts = p.partials + row * gridDim.x;
   if (threadIdx.x == 0) {
     __stcg(parts + blockIdx.x, pack(cta));
-    __threadfence();
-    const unsigned t = atomicAdd(p.tickets + row, 1u);
-    s_last = (t == gridDim.x - 1);
+    s_last = (ticket_acq_rel(p.tickets + row) == gridDim.x - 1);
   }
   __syncthreads();
   if (!s_last) return;
-  __threadfence();
   A v = R::id();
   for (int i = threadIdx.x; i < (int)gridDim.x; i += BLOCK) v = R::op(v, unpack<A>(__ldcg(parts + i)));
   __syncthreads();  // sm reuse
@@ -370,10 +375,11 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_flat_guided(FlatParams 
   const int64_t dyn0 = srounds * G;
   const int64_t rem = ntiles - dyn0;
   const int64_t max_chunks = p.max_chunks > 0 ? p.max_chunks : 1;
-  // tiles per dynamic chunk: enough chunks to balance, >= 4 tiles each to amortise the per-chunk block
-  // reduction (tools/sweep_flat.cu "chunks": 1-tile chunks cost 2.6% at 1 GiB)
+  // tiles per dynamic chunk: enough chunks to balance; >= 4 tiles each to amortise the per-chunk block
+  // reduction when there are at least 4 such chunks per CTA (tools/sweep_flat.cu "chunks": 1-tile chunks cost
+  // 2.6% at 1 GiB), single tiles for small inputs (few chunks would leave most CTAs idle)
   int64_t ct = rem > 0 ? (rem + max_chunks - 1) / max_chunks : 1;
-  if (ct < 4) ct = 4;
+  if (ct < 4 && rem >= 16 * G) ct = 4;
   const int64_t K = (rem + ct - 1) / ct;                 // dynamic chunks 0..K-1; chunk K = the remainder
   uint64_t* slots = p.partials;
 
@@ -465,13 +471,9 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_flat_guided(FlatParams 
     c = s_c;
   }
   // the CTA that takes the last ticket folds all slots (fixed thread -> slot mapping and tree)
-  if (threadIdx.x == 0) {
-    __threadfence();
-    s_last = atomicAdd(p.tickets, 1u) == gridDim.x - 1;
-  }
+  if (threadIdx.x == 0) s_last = ticket_acq_rel(p.tickets) == gridDim.x - 1;
   __syncthreads();
   if (!s_last) return;
-  __threadfence();
   const int64_t nslots = G + K + 1;
   A v = R::id();
   for (int64_t i = threadIdx.x; i < nslots; i += BLOCK) v = R::op(v, unpack<A>(__ldcg(slots + i)));
