@@ -12,7 +12,7 @@ flush is needed between steps. Timed with CUDA events between two barriers, max 
 Rank 0 prints ONE JSON line. Besides the contract keys it carries:
   roofline      the flat kernel's HBM roofline: algorithmic bytes per launch / its live per-launch event time
   cpu_baseline  the CPU oracle (test infrastructure, tests/ + here only) timed on a bounded sample, 1 core
-  e2e           the same metric through ipm_reduce_host: pinned host shard -> device inside the timed region
+  e2e           the same metric through ipm_reduce_host_dist: pinned host shards -> devices + the rank exchange
   suite         (N=1) the other BASELINE configs device-timed: C1 latency, C2 per op, C3 segmented, C4 per op
 `--impl reference` times the CPU oracle as the reference arm on the same metric (no GPU work).
 """
@@ -411,13 +411,13 @@ def run_ours(args, rank, world, local_rank):
             del x
             torch.cuda.empty_cache()
             for _ in range(1):
-                ipm.reduce_host("+", host, init=init, ws=ws)  # warm (allocates the staging buffers)
+                comm.reduce_host("+", host, init=init, ws=ws)  # warm (allocates the staging buffers)
             barrier()
             t0 = torch.cuda.Event(enable_timing=True)
             t1 = torch.cuda.Event(enable_timing=True)
             t0.record(stream)
-            for _ in range(e2e_steps):
-                part = ipm.reduce_host("+", host, init=init, ws=ws)  # local shard, D2H of the result
+            for _ in range(e2e_steps):  # every rank: its pinned host shard -> device, exchange, global result
+                part = comm.reduce_host("+", host, init=init, ws=ws)
             t1.record(stream)
             t1.synchronize()
             barrier()
@@ -426,8 +426,9 @@ def run_ours(args, rank, world, local_rank):
                 dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
             e2e = {"value": total_bytes / (float(e_ms.item()) / 1e3) / 1e9, "unit": "GB/s",
                    "h2d_bytes_per_step": total_bytes, "d2h_bytes_per_step": 4 * world, "steps": e2e_steps,
-                   "ms_per_step": float(e_ms.item()), "path": "ipm_reduce_host: pinned host shard, 64 MiB chunks "
-                   "double-buffered H2D overlapped with the reduce kernels", "host_result_rank0": float(part)}
+                   "ms_per_step": float(e_ms.item()), "path": "ipm_reduce_host_dist: pinned host shard per rank, 64 MiB "
+                   "chunks double-buffered H2D overlapped with the reduce kernels, then the rank exchange",
+                   "host_result_rank0": float(part)}
             del host
             ipm.lib.ipm_release_staging()
         except Exception as ex:  # pinned allocation can fail on small hosts: say so, keep the device number

@@ -257,6 +257,12 @@ ipm_status ipm_shard_range(int64_t n, int rank, int world, int64_t* lo, int64_t*
  * the global result (out). Blocks until *inout is written. */
 ipm_status ipm_reduce_dist(ipm_comm* comm, ipm_op op, ipm_dtype dt, const void* dev_shard, int64_t n_shard,
                            void* inout, void* workspace, void* stream);
+/* End-to-end multi-GPU clause over HOST shards: each rank's host_shard (n_shard elements, pinned fastest) is
+ * streamed to its device through the staging ring of ipm_reduce_host and folded into an accumulator partial on
+ * the device, then the partials are exchanged exactly as in ipm_reduce_dist. inout: host scalar, the same init on
+ * every rank (in) and the global result (out). Blocks until *inout is written. */
+ipm_status ipm_reduce_host_dist(ipm_comm* comm, ipm_op op, ipm_dtype dt, const void* host_shard, int64_t n_shard,
+                                void* inout, void* workspace, void* stream);
 /* 1 if ipm_reduce_dist on this communicator takes the fused path: every peer's symmetric slot buffer is mapped
  * (CUDA IPC over NVLink) and IPM_OPT_DIST_MODE is 0 — the reduction kernel then exchanges the rank partials
  * itself (one kernel per rank per call). 0: ncclAllGather + a one-warp fold kernel. */

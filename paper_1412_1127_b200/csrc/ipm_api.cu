@@ -198,6 +198,9 @@ struct Launch {
       default: k_seg_group<R, 16><<<grid, 256, 0, st>>>(p); break;
     }
   }
+  static void exchange(const FlatParams& p, const uint64_t* acc, cudaStream_t st) {
+    k_exchange<R><<<1, 32, 0, st>>>(p, acc);
+  }
   static void finalize(const uint64_t* slots, int P, uint64_t init, int has_init, void* out, cudaStream_t st) {
     k_finalize<R><<<1, 32, 0, st>>>(slots, P, init, has_init, out);
   }
@@ -211,13 +214,14 @@ struct Table {
   cudaError_t (*seg_tma)(const SegParams&, int, cudaStream_t);
   void (*seg_group)(const SegParams&, int, int, cudaStream_t);
   void (*finalize)(const uint64_t*, int, uint64_t, int, void*, cudaStream_t);
+  void (*exchange)(const FlatParams&, const uint64_t*, cudaStream_t);
 };
 
 static const Table* table(ipm_op op, ipm_dtype dt) {
 #define IPM_ENTRY(O, D)                                                                                  \
   if (op == O && dt == D) {                                                                            \
     static const Table t = {&Launch<O, D>::flat, &Launch<O, D>::two_d, &Launch<O, D>::ragged, &Launch<O, D>::seg_warp, &Launch<O, D>::seg_tma,     \
-                            &Launch<O, D>::seg_group, &Launch<O, D>::finalize};                        \
+                            &Launch<O, D>::seg_group, &Launch<O, D>::finalize, &Launch<O, D>::exchange};\
     return &t;                                                                                         \
   }
   IPM_LEGAL(IPM_ENTRY)
@@ -280,6 +284,23 @@ ipm_status launch_flat(ipm_op op, ipm_dtype dt, const void* dev, int64_t n, uint
 ipm_status launch_finalize(ipm_op op, ipm_dtype dt, const uint64_t* slots, int P, uint64_t init, int has_init,
                            void* out, cudaStream_t st) {
   table(op, dt)->finalize(slots, P, init, has_init, out, st);
+  CK(cudaGetLastError());
+  return IPM_OK;
+}
+
+ipm_status launch_exchange(ipm_op op, ipm_dtype dt, const uint64_t* acc, uint64_t init, int has_init, void* out,
+                           const DistArgs* dist, cudaStream_t st) {
+  FlatParams p;
+  memset(&p, 0, sizeof p);
+  p.init = init;
+  p.has_init = has_init;
+  p.mode = MODE_DIST;
+  p.out = out;
+  p.peers = dist->peers;
+  p.rank = dist->rank;
+  p.world = dist->world;
+  p.timeout_ns = dist->timeout_ns;
+  table(op, dt)->exchange(p, acc, st);
   CK(cudaGetLastError());
   return IPM_OK;
 }
@@ -866,6 +887,60 @@ ipm_status ipm_release_staging(void) {
   return release_staging_locked();
 }
 
+}  // extern "C"
+
+namespace ipm {
+// copyin fused with the reduction: the host array streams through two staging buffers (H2D of chunk c+1 on a
+// copy stream overlapping the kernel of chunk c); each chunk's kernel folds into the running accumulator at
+// ws + WS_ACC (MODE_ACCUM), so the partial of the whole array stays on the device
+ipm_status stream_host_partial(ipm_op op, ipm_dtype dt, const void* host, int64_t n, void* ws, cudaStream_t st) {
+  ipm_status s;
+  const size_t es = esize(dt);
+  uint64_t* acc = (uint64_t*)((char*)ws + WS_ACC);
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (n == 0) return launch_flat(op, dt, nullptr, 0, 0, 0, MODE_ACCUM_FIRST, acc, ws, st);  // identity
+  const size_t chunk_bytes = (size_t)std::max(1, env_int("IPM_STAGE_MB", 64)) << 20;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  if (g_stage.device != dev || g_stage.bytes != chunk_bytes) {
+    release_staging_locked();
+    CK(cudaStreamCreateWithFlags(&g_stage.copy, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      CK(cudaEventCreateWithFlags(&g_stage.copied[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&g_stage.consumed[i], cudaEventDisableTiming));
+      g_stage.buf[i] = dev_alloc(chunk_bytes, g_stage.copy);
+      if (!g_stage.buf[i]) {
+        release_staging_locked();
+        set_error("staging allocation failed");
+        return IPM_E_CUDA;
+      }
+    }
+    CK(cudaStreamSynchronize(g_stage.copy));
+    g_stage.bytes = chunk_bytes;
+    g_stage.device = dev;
+  }
+  const int64_t per = (int64_t)(chunk_bytes / es);
+  // the staging buffers are free once everything previously queued on `st` has run
+  for (int i = 0; i < 2; ++i) CK(cudaEventRecord(g_stage.consumed[i], st));
+  int64_t c = 0;
+  for (int64_t off = 0; off < n; off += per, ++c) {
+    const int b = (int)(c & 1);
+    const int64_t cnt = std::min(per, n - off);
+    CK(cudaStreamWaitEvent(g_stage.copy, g_stage.consumed[b], 0));
+    CK(cudaMemcpyAsync(g_stage.buf[b], (const char*)host + off * es, cnt * es, cudaMemcpyHostToDevice,
+                       g_stage.copy));
+    CK(cudaEventRecord(g_stage.copied[b], g_stage.copy));
+    CK(cudaStreamWaitEvent(st, g_stage.copied[b], 0));
+    if ((s = launch_flat(op, dt, g_stage.buf[b], cnt, 0, 0, c == 0 ? MODE_ACCUM_FIRST : MODE_ACCUM, acc, ws, st)))
+      return s;
+    CK(cudaEventRecord(g_stage.consumed[b], st));
+  }
+  return IPM_OK;
+}
+}  // namespace ipm
+
+extern "C" {
+
 ipm_status ipm_reduce_host(ipm_op op, ipm_dtype dt, const void* host, int64_t n, void* inout, void* ws,
                            void* stream) {
   ipm_status s;
@@ -879,54 +954,11 @@ ipm_status ipm_reduce_host(ipm_op op, ipm_dtype dt, const void* host, int64_t n,
     return IPM_E_NULL;
   }
   cudaStream_t st = (cudaStream_t)stream;
-  const size_t es = esize(dt);
-  const uint64_t ib = scalar_bits(dt, inout);
   void* res = (char*)ws + WS_RESULT;
-  uint64_t* acc = (uint64_t*)((char*)ws + WS_ACC);
-  std::lock_guard<std::mutex> lk(g_mu);
-  if (n == 0) {
-    if ((s = launch_finalize(op, dt, nullptr, 0, ib, 1, res, st))) return s;
-  } else {
-    const size_t chunk_bytes = (size_t)std::max(1, env_int("IPM_STAGE_MB", 64)) << 20;
-    int dev = 0;
-    CK(cudaGetDevice(&dev));
-    if (g_stage.device != dev || g_stage.bytes != chunk_bytes) {
-      release_staging_locked();
-      CK(cudaStreamCreateWithFlags(&g_stage.copy, cudaStreamNonBlocking));
-      for (int i = 0; i < 2; ++i) {
-        CK(cudaEventCreateWithFlags(&g_stage.copied[i], cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&g_stage.consumed[i], cudaEventDisableTiming));
-        g_stage.buf[i] = dev_alloc(chunk_bytes, g_stage.copy);
-        if (!g_stage.buf[i]) {
-          release_staging_locked();
-          set_error("staging allocation failed");
-          return IPM_E_CUDA;
-        }
-      }
-      CK(cudaStreamSynchronize(g_stage.copy));
-      g_stage.bytes = chunk_bytes;
-      g_stage.device = dev;
-    }
-    const int64_t per = (int64_t)(chunk_bytes / es);
-    // the staging buffers are free once everything previously queued on `st` has run
-    for (int i = 0; i < 2; ++i) CK(cudaEventRecord(g_stage.consumed[i], st));
-    int64_t c = 0;
-    for (int64_t off = 0; off < n; off += per, ++c) {
-      const int b = (int)(c & 1);
-      const int64_t cnt = std::min(per, n - off);
-      CK(cudaStreamWaitEvent(g_stage.copy, g_stage.consumed[b], 0));
-      CK(cudaMemcpyAsync(g_stage.buf[b], (const char*)host + off * es, cnt * es, cudaMemcpyHostToDevice,
-                         g_stage.copy));
-      CK(cudaEventRecord(g_stage.copied[b], g_stage.copy));
-      CK(cudaStreamWaitEvent(st, g_stage.copied[b], 0));
-      if ((s = launch_flat(op, dt, g_stage.buf[b], cnt, 0, 0, c == 0 ? MODE_ACCUM_FIRST : MODE_ACCUM, acc, ws,
-                           st)))
-        return s;
-      CK(cudaEventRecord(g_stage.consumed[b], st));
-    }
-    if ((s = launch_finalize(op, dt, acc, 1, ib, 1, res, st))) return s;
-  }
-  CK(cudaMemcpyAsync(inout, res, es, cudaMemcpyDeviceToHost, st));
+  if ((s = stream_host_partial(op, dt, host, n, ws, st))) return s;
+  if ((s = launch_finalize(op, dt, (const uint64_t*)((char*)ws + WS_ACC), 1, scalar_bits(dt, inout), 1, res, st)))
+    return s;
+  CK(cudaMemcpyAsync(inout, res, esize(dt), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   return IPM_OK;
 }

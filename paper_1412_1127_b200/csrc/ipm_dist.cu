@@ -267,6 +267,47 @@ ipm_status ipm_reduce_dist(ipm_comm* comm, ipm_op op, ipm_dtype dt, const void* 
   return IPM_OK;
 }
 
+ipm_status ipm_reduce_host_dist(ipm_comm* comm, ipm_op op, ipm_dtype dt, const void* host_shard, int64_t n_shard,
+                                void* inout, void* ws, void* stream) {
+  ipm_status s;
+  if (!comm || !inout || (n_shard > 0 && !host_shard)) {
+    set_error("NULL pointer");
+    return IPM_E_NULL;
+  }
+  if ((s = validate(op, dt))) return s;
+  if (n_shard < 0) {
+    set_error("negative element count");
+    return IPM_E_SIZE;
+  }
+  if (!ws || ((uintptr_t)ws & 255u)) {
+    set_error("workspace must be a non-NULL, 256-byte aligned device buffer");
+    return IPM_E_WORKSPACE;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if ((s = stream_host_partial(op, dt, host_shard, n_shard, ws, st))) return s;
+  const uint64_t* acc = (const uint64_t*)((char*)ws + WS_ACC);
+  void* res = (char*)ws + WS_RESULT;
+  const uint64_t ib = scalar_bits(dt, inout);
+  if (comm->p2p && (dist_mode_option() == 0 || !comm->nccl)) {
+    DistArgs d{comm->peers_dev, comm->rank, comm->world, dist_timeout_ns()};
+    if ((s = launch_exchange(op, dt, acc, ib, 1, res, &d, st))) return s;
+  } else {
+    uint64_t* slots = (uint64_t*)((char*)ws + WS_SLOTS);
+    ncclResult_t r = ncclAllGather(acc, slots, 1, ncclUint64, comm->nccl, st);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather");
+    if ((s = launch_finalize(op, dt, slots, comm->world, ib, 1, res, st))) return s;
+  }
+  cudaError_t e = cudaMemcpyAsync(inout, res, esize(dt), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "ipm_reduce_host_dist");
+  int err = 0;
+  if (comm->p2p && ipm_comm_error(comm, &err) == IPM_OK && err) {
+    set_error("fused exchange: a peer did not arrive within the timeout (result undefined)");
+    return IPM_E_NCCL;
+  }
+  return IPM_OK;
+}
+
 int ipm_comm_uses_peer_memory(const ipm_comm* comm) {
   return comm && comm->p2p && (dist_mode_option() == 0 || !comm->nccl);
 }

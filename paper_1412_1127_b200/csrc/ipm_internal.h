@@ -41,6 +41,10 @@ struct DistArgs {             // L_DIST: the fused multi-GPU exchange (ipm_kerne
 };
 ipm_status launch_flat(ipm_op op, ipm_dtype dt, const void* dev, int64_t n, uint64_t init, int has_init, int mode,
                        void* out, void* ws, cudaStream_t st, const DistArgs* dist = nullptr);
+ipm_status launch_exchange(ipm_op op, ipm_dtype dt, const uint64_t* acc, uint64_t init, int has_init, void* out,
+                           const DistArgs* dist, cudaStream_t st);
+// host-streaming copyin fused with the reduction: leaves the accumulator partial of host[0..n) at ws + WS_ACC
+ipm_status stream_host_partial(ipm_op op, ipm_dtype dt, const void* host, int64_t n, void* ws, cudaStream_t st);
 int dist_mode_option();       // IPM_OPT_DIST_MODE: 0 auto (peer memory when mapped), 1 NCCL
 long long dist_timeout_ns();
 ipm_status launch_finalize(ipm_op op, ipm_dtype dt, const uint64_t* slots, int P, uint64_t init, int has_init,

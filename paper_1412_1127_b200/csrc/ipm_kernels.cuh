@@ -765,6 +765,14 @@ __global__ void __launch_bounds__(256) k_seg_group(SegParams p) {
   }
 }
 
+// ------------------------------------------------------------------------------------------ exchange
+// the multi-GPU exchange of an accumulator partial already in device memory (host-streaming path): one
+// thread runs the same store_out as the reduction kernels (MODE_DIST: dist_exchange)
+template <class R>
+__global__ void __launch_bounds__(32) k_exchange(FlatParams p, const uint64_t* acc) {
+  if (threadIdx.x == 0) store_out<R>(p, 0, unpack<typename R::A>(__ldcg(acc)));
+}
+
 // ------------------------------------------------------------------------------------------ finalize
 // out = fin(init ⊕ slot[0] ⊕ ... ⊕ slot[P-1]) — cross-rank (a9) or cross-chunk fold, in slot order groups
 template <class R>

@@ -81,6 +81,7 @@ def _load():
         "ipm_shard_range": ([i64, ci, ci, ctypes.POINTER(i64), ctypes.POINTER(i64)], ci),
         "ipm_comm_uses_peer_memory": ([vp], ci),
         "ipm_comm_error": ([vp, ctypes.POINTER(ci)], ci),
+        "ipm_reduce_host_dist": ([vp, ci, ci, vp, i64, vp, vp, vp], ci),
         "ipm_reduce_dist": ([vp, ci, ci, vp, i64, vp, vp, vp], ci),
         "ipm_reduce_dist_async": ([vp, ci, ci, vp, i64, vp, vp, vp, vp], ci),
     }
@@ -98,7 +99,7 @@ EXPORTED = ("ipm_status_str ipm_last_error_message ipm_op_legal ipm_dtype_size i
             "ipm_reduce_segmented ipm_reduce_ragged ipm_reduce_partials ipm_finalize_partials ipm_reduce_2d ipm_reduce_2d_async ipm_fused_nvars ipm_reduce_fused ipm_reduce_fused_async ipm_reduce_host ipm_release_staging ipm_set_option ipm_profile_enable ipm_profile_read "
             "ipm_profile_disable ipm_flat_geometry ipm_comm_id_bytes "
             "ipm_comm_unique_id ipm_comm_init ipm_comm_destroy ipm_comm_init_group ipm_shard_range ipm_comm_uses_peer_memory ipm_comm_error "
-            "ipm_reduce_dist "
+            "ipm_reduce_host_dist ipm_reduce_dist "
             "ipm_reduce_dist_async").split()
 
 
@@ -579,6 +580,26 @@ class Comm:
             return out.cpu().numpy()[0]
         _check(lib.ipm_reduce_dist(self._h, op_code(op), dt, ptr, n, box.ctypes.data, ws.data_ptr(),
                                    _stream(stream)), "ipm_reduce_dist")
+        return box[0]
+
+    def reduce_host(self, op: str, host_shard, init=None, ws: torch.Tensor | None = None, stream=None):
+        """End to end: this rank's HOST shard (numpy array or CPU tensor, pinned fastest) is streamed to the GPU,
+        reduced and exchanged (ipm_reduce_host_dist); every rank returns the global result."""
+        if isinstance(host_shard, torch.Tensor):
+            if host_shard.is_cuda:
+                raise ValueError("reduce_host takes a host array")
+            keep = host_shard.contiguous()
+            ptr, n, dt = keep.data_ptr(), keep.numel(), DTYPES[keep.dtype]
+        else:
+            keep = np.ascontiguousarray(host_shard)
+            ptr, n, dt = keep.ctypes.data, keep.size, dtype_code(keep.dtype)
+        ws = workspace(stream) if ws is None else ws
+        box = _scalar(dt, init)
+        if box is None:
+            box = _scalar(dt, identity_value(op, dt))
+        _check(lib.ipm_reduce_host_dist(self._h, op_code(op), dt, ptr, n, box.ctypes.data, ws.data_ptr(),
+                                        _stream(stream)), "ipm_reduce_host_dist")
+        del keep
         return box[0]
 
     def reduce_async(self, op: str, shard: torch.Tensor, init=None, out: torch.Tensor | None = None,

@@ -296,6 +296,8 @@ def test_dist_world1(ipm, mode):
             # an empty shard contributes the identity
             check(op, dt, comm.reduce(op, x[:0], init=NPT[dt](1)), *oracle.reduce(op, x[:0].cpu().numpy(),
                                                                                  init=NPT[dt](1)))
+            # end to end from a host shard (copyin fused with the reduction, then the exchange)
+            check(op, dt, comm.reduce_host(op, ipmgen.fill_host(spec), init=NPT[dt](1)), want_t, want_ld)
         comm.close()
     finally:
         ipm.set_option("dist_mode", "auto")
