@@ -164,7 +164,9 @@ struct Launch {
   // then differ in the last bits between runs). Multi-row launches (grid.y > 1) and the per-block partials
   // mode keep the static grid-stride schedule.
   static void flat(const FlatParams& p, dim3 grid, cudaStream_t st) {
-    if (p.counter && grid.y == 1 && grid.x > 1 && g_opt_deterministic != 2) {
+    // up to 64 MiB the launch is latency-bound: the static schedule saves the chunk claims (C1: 12.4 -> 10.3 us)
+    const bool small = p.n * (int64_t)sizeof(typename R::B) <= (64ll << 20);
+    if (p.counter && grid.y == 1 && grid.x > 1 && g_opt_deterministic != 2 && !small) {
       if (g_opt_deterministic) k_flat_guided<R, FLAT_BLOCK, GUIDED_U, true><<<grid, FLAT_BLOCK, 0, st>>>(p);
       else k_flat<R, FLAT_BLOCK, FLAT_U, 0, 2><<<grid, FLAT_BLOCK, 0, st>>>(p);
     } else {
