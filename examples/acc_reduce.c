@@ -11,6 +11,7 @@
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
+#include <time.h>
 
 #include <cuda_runtime_api.h>
 
@@ -68,6 +69,22 @@ int main(void) {
     void* sub = NULL;
     CHECK(ipm_present(a + 100, 4 * sizeof(int32_t), &sub));
     if ((char*)sub != (char*)dev + 100 * sizeof(int32_t)) failures++;
+  }
+  /* host-side latency of the synchronous clause on BASELINE config 1 (2^20 int32): launch + kernel + 4-byte D2H */
+  {
+    const int64_t n1 = (int64_t)1 << 20;
+    struct timespec t0, t1;
+    int r, reps = 2000;
+    for (r = 0; r < 100; ++r) CHECK(ipm_reduce(IPM_ADD, IPM_I32, dev, n1, &x, ws, NULL));
+    clock_gettime(CLOCK_MONOTONIC, &t0);
+    for (r = 0; r < reps; ++r) {
+      x = 0;
+      CHECK(ipm_reduce(IPM_ADD, IPM_I32, dev, n1, &x, ws, NULL));
+    }
+    clock_gettime(CLOCK_MONOTONIC, &t1);
+    printf("ipm_reduce(+, 2^20 int32) synchronous call: %.2f us (L2-warm)\n",
+           ((t1.tv_sec - t0.tv_sec) * 1e9 + (t1.tv_nsec - t0.tv_nsec)) / 1e3 / reps);
+    if (x != (int32_t)(((uint64_t)n1 * (uint64_t)(n1 + 1) / 2) & 0xFFFFFFFFu)) failures++;
   }
   CHECK(ipm_delete(a, NULL));
   if (ipm_present_count() != 0) failures++;
