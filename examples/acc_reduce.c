@@ -8,6 +8,7 @@
  *   gcc -std=c99 -O2 -Wall -Werror -pedantic -I include -isystem /usr/local/cuda/include examples/acc_reduce.c \
  *       -L paper_1412_1127_b200 -lipm -Wl,-rpath,$PWD/paper_1412_1127_b200 -L/usr/local/cuda/lib64 -lcudart
  * Exit status 0 iff every result matches its closed form. */
+#define _POSIX_C_SOURCE 199309L
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
