@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_flat_guided(FlatParams 
   // reduction when there are at least 4 such chunks per CTA (tools/sweep_flat.cu "chunks": 1-tile chunks cost
   // 2.6% at 1 GiB), single tiles for small inputs (few chunks would leave most CTAs idle)
   int64_t ct = rem > 0 ? (rem + max_chunks - 1) / max_chunks : 1;
-  if (ct < 4 && rem >= 16 * G) ct = 4;
+  if (ct < 4 && rem >= 4 * G) ct = 4;
   const int64_t K = (rem + ct - 1) / ct;                 // dynamic chunks 0..K-1; chunk K = the remainder
   uint64_t* slots = p.partials;
 
@@ -475,9 +475,23 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_flat_guided(FlatParams 
   __syncthreads();
   if (!s_last) return;
   const int64_t nslots = G + K + 1;
-  A v = R::id();
-  for (int64_t i = threadIdx.x; i < nslots; i += BLOCK) v = R::op(v, unpack<A>(__ldcg(slots + i)));
-  const A total = block_reduce<R, BLOCK>(v, sm);
+  // thousands of slots: 8 independent loads in flight per thread (a dependent load-op chain would cost one L2
+  // round trip per slot); fixed thread -> slot mapping and combine order
+  A v8[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) v8[j] = R::id();
+  int64_t i = threadIdx.x;
+  for (; i + 7 * BLOCK < nslots; i += 8 * BLOCK) {
+    uint64_t w[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) w[j] = __ldcg(slots + i + j * BLOCK);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v8[j] = R::op(v8[j], unpack<A>(w[j]));
+  }
+  for (int j = 0; i < nslots; i += BLOCK, ++j) v8[j & 7] = R::op(v8[j & 7], unpack<A>(__ldcg(slots + i)));
+#pragma unroll
+  for (int j = 1; j < 8; ++j) v8[0] = R::op(v8[0], v8[j]);
+  const A total = block_reduce<R, BLOCK>(v8[0], sm);
   if (threadIdx.x == 0) {
     store_out<R>(p, 0, total);
     *p.tickets = 0u;
