@@ -204,7 +204,10 @@ def _flat_arg(t: torch.Tensor):
 # ------------------------------------------------------------------ reductions
 def reduce(op: str, t: torch.Tensor, init=None, ws: torch.Tensor | None = None, stream=None):
     """`reduction(op:var)` over all elements of a CUDA tensor; returns init ⊕ fold as a numpy scalar.
-    Blocks until the result is on the host (ipm_reduce)."""
+    Blocks until the result is on the host (ipm_reduce). A non-contiguous 2-D view whose rows are contiguous
+    (e.g. ``big[:, a:b]``) is reduced in place as a strided 2-D region (ipm_reduce_2d)."""
+    if t.is_cuda and not t.is_contiguous() and t.dim() == 2 and (t.shape[1] <= 1 or t.stride(1) == 1):
+        return reduce_2d(op, t, init=init, ws=ws, stream=stream)
     ptr, n, dt = _flat_arg(t)
     s = _stream(stream)
     ws = workspace(stream) if ws is None else ws

@@ -384,6 +384,7 @@ def test_2d_view_api(ipm):
     sub = big[10:900, 33:650]
     assert ipm.reduce_2d("+", sub) == int(sub.sum())
     assert ipm.reduce_2d("max", sub) == int(sub.max())
+    assert ipm.reduce("^", sub) == int(np.bitwise_xor.reduce(sub.cpu().numpy().ravel()))   # reduce() dispatches
 
 
 # --------------------------------------------------------------------------- ragged (CSR) rows
