@@ -177,7 +177,12 @@ struct Launch {
     k_seg_warp<R, SEG_WARPS, SEG_U><<<grid, SEG_WARPS * 32, 0, st>>>(p);
   }
   static void ragged(const RaggedParams& p, int blocks, int64_t nw, cudaStream_t st) {
-    k_ragged_vec<R, 8, 4, 2><<<blocks, 256, 0, st>>>(p);  // 4 CTAs x 8 warps per SM, 2 vectors per lane
+    // 25 KiB of static shared memory per CTA: ask for the largest carveout so 8 CTAs fit on an SM
+    static const bool carveout = cudaFuncSetAttribute(k_ragged_vec<R, 4, 8, 2>,
+                                                      cudaFuncAttributePreferredSharedMemoryCarveout,
+                                                      (int)cudaSharedmemCarveoutMaxShared) == cudaSuccess;
+    (void)carveout;
+    k_ragged_vec<R, 4, 8, 2><<<blocks, 128, 0, st>>>(p);  // 8 CTAs x 4 warps per SM, 2 vectors per lane
     k_ragged_fix<R><<<(unsigned)((nw + 7) / 8), 256, 0, st>>>(p, nw);
   }
   static void two_d(const Params2D& q, int grid, cudaStream_t st) {
@@ -729,7 +734,7 @@ ipm_status ipm_reduce_ragged(ipm_op op, ipm_dtype dt, const void* dev, const int
   p.init = scalar_bits(dt, init);
   p.has_init = init != nullptr;
   p.out = dev_out;
-  const int64_t nw = std::min<int64_t>((int64_t)sm_count() * 32, WS_MAX_RAGGED_WARPS);  // 4 CTAs x 8 warps per SM
+  const int64_t nw = std::min<int64_t>((int64_t)sm_count() * 32, WS_MAX_RAGGED_WARPS);  // 8 CTAs x 4 warps per SM
   int64_t* base = (int64_t*)((char*)ws + WS_RAGGED);
   p.head_row = base;
   p.head_part = (uint64_t*)(base + WS_MAX_RAGGED_WARPS);
@@ -738,7 +743,7 @@ ipm_status ipm_reduce_ragged(ipm_op op, ipm_dtype dt, const void* dev, const int
   cudaStream_t st = (cudaStream_t)stream;
   {
     ProfScope ps(st, 4);
-    table(op, dt)->ragged(p, (int)(nw / 8), nw, st);
+    table(op, dt)->ragged(p, (int)(nw / 4), nw, st);
   }
   CK(cudaGetLastError());
   return IPM_OK;

@@ -871,10 +871,14 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_vec(RaggedParams p)
   constexpr int EPL = VW * VPL;  // elements per lane per chunk (<= 32: one flag bit each)
   constexpr int CH = 32 * EPL;   // elements per chunk
   static_assert(EPL <= 32, "flag word");
+  // per warp, column-major by lane (position EPL*l + k at [k*32 + l]: a lane's column is bank-conflict free)
   __shared__ int s_rid[WARPS][CH];        // chunk position -> (row - r0) starting there (valid where flagged)
+  __shared__ A s_val[WARPS][CH];          // value of the segment that ends just before a flagged position
   __shared__ unsigned s_flag[WARPS][32];  // per lane: bit k = a row starts at the lane's element k
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int* rid_map = s_rid[wid];
+  const int* rid_col = s_rid[wid] + lane;
+  A* val_col = s_val[wid] + lane;
   unsigned* flagw = s_flag[wid];
   flagw[lane] = 0u;
   const unsigned lanemask_lt = (1u << lane) - 1u;
@@ -947,7 +951,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_vec(RaggedParams p)
         const bool inr = r < p.rows && d >= rlo_c && d < rhi_c;
         if (inr && ew > sw) {
           const int rel = (int)d;
-          rid_map[rel] = (int)(r - r0);
+          rid_map[(rel % EPL) * 32 + rel / EPL] = (int)(r - r0);
           atomicOr(&flagw[rel / EPL], 1u << (rel % EPL));
         }
         if (inr && ew == sw) finish(r, R::id());
@@ -965,44 +969,39 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_vec(RaggedParams p)
       __syncwarp();
       const unsigned fl = flagw[lane];
       flagw[lane] = 0u;
-      // lane-local fold: head = elements before the first flag, tail = from the last flag on; rows that start
-      // and end inside this lane (two or more flags) are finished separately
-      A xv[EPL];
+      // lane-local segmented fold, one pass: at every flagged element the running value (the segment that
+      // ends there) is parked in the lane's own shared-memory column and the accumulator restarts
+      A acc = R::id();
       if (interior) {
 #pragma unroll
-        for (int k = 0; k < EPL; ++k) xv[k] = R::lift(x[k]);
+        for (int k = 0; k < EPL; ++k) {
+          const bool s = (fl >> k) & 1u;
+          if (s) val_col[k * 32] = acc;
+          acc = R::op(s ? R::id() : acc, R::lift(x[k]));
+        }
       } else {
 #pragma unroll
         for (int k = 0; k < EPL; ++k) {
           const int rel = EPL * lane + k;
-          xv[k] = (rel >= rlo_c && rel < rhi_c) ? R::lift(x[k]) : R::id();
+          const bool s = (fl >> k) & 1u;
+          if (s) val_col[k * 32] = acc;
+          acc = R::op(s ? R::id() : acc, (rel >= rlo_c && rel < rhi_c) ? R::lift(x[k]) : R::id());
         }
       }
       const int kf = fl ? __ffs(fl) - 1 : EPL;
       const int kl = fl ? 31 - __clz(fl) : EPL;
-      A head = R::id(), cur = R::id();
-#pragma unroll
-      for (int k = 0; k < EPL; ++k) {
-        if (k < kf) head = R::op(head, xv[k]);
-        if (k >= kl) cur = R::op(cur, xv[k]);
-      }
-      if (__popc(fl) >= 2) {  // whole rows inside this lane
-        unsigned m = fl & ~(1u << kl);
-        while (m) {
-          const int k0 = __ffs(m) - 1;
-          m &= m - 1;
-          const unsigned rest = fl & ~((2u << k0) - 1u);
-          const int k1 = __ffs(rest) - 1;
-          A v = R::id();
-#pragma unroll
-          for (int k = 0; k < EPL; ++k)
-            if (k >= k0 && k < k1) v = R::op(v, xv[k]);
-          finish(r0 + rid_map[EPL * lane + k0], v);
-        }
+      // head = elements before the first flag, cur = from the last flag on
+      const A head = fl ? val_col[kf * 32] : acc;
+      const A cur = fl ? acc : R::id();
+      // rows that start and end inside this lane: between consecutive flags, value parked at the later one
+      for (unsigned m = fl & ~(1u << kl); m; m &= m - 1) {
+        const int k0 = __ffs(m) - 1;
+        const int k1 = __ffs(fl & ~((2u << k0) - 1u)) - 1;
+        finish(r0 + rid_col[k0 * 32], val_col[k1 * 32]);
       }
       const bool flag = fl != 0u;
       const int lastk = kl;
-      const long long my_rid = flag ? (long long)(r0 + rid_map[EPL * lane + lastk]) : -1;
+      const long long my_rid = flag ? (long long)(r0 + rid_col[lastk * 32]) : -1;
       // segmented inclusive scan over lanes: a flagged lane starts a segment with its tail value
       const unsigned bal = __ballot_sync(FULL, flag);
       const unsigned le = bal & (lanemask_lt | (1u << lane));

@@ -50,7 +50,10 @@ def test_c2(ipm, op, dt):
         assert abs(np.longdouble(got) - want_ld) <= TOL[dt] * abs(want_ld)
     else:
         assert got == want_t
-    if op == "+":  # dyadic grid: every partial sum is exact in fp64 -> the correctly rounded sum
+    if op == "+" and dt == "float32":
+        # float32 data on a 2^-14 grid below 2^10 summed in fp64: every partial sum (< 2^38 units of 2^-14, 52
+        # bits) is exact -> the correctly rounded sum. float64 data (2^-43 grid) needs 81 bits, so
+        # float64 sums round and only the 1e-12 bound above applies (DESIGN.md R-tolerance).
         assert got == NPT[dt](want_ld)
 
 
