@@ -912,16 +912,25 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_vec(RaggedParams p)
     const int64_t n0 = __shfl_sync(FULL, nxt0, 0);
     return lane == 31 ? n0 : up;
   };
-  int64_t sw = fetch(wb);
+  // chunk bases: positions whose address is 32-byte aligned, from q0; window quantities are kept relative to q0
+  // in 32 bits (clamped: a row starting past the warp's range only needs to compare as "later")
+  const int64_t q0 = lo - (int64_t)(((uintptr_t)(a + lo) & 31u) / sizeof(B));
   int64_t nx = fetch(wb + 32);   // the next window
   int64_t nx2 = fetch(wb + 64);  // and the one after (its first offset closes the next window's last row)
-  int64_t ew = ends(sw, nx);
+  int wpos;                      // off[wb + lane] - q0
+  bool wrow, wfull;              // wb + lane is a row; it is non-empty
+  auto window = [&](int64_t sw) {
+    const int64_t ew = ends(sw, nx);
+    const int64_t d = sw - q0;
+    wpos = d < (int64_t)INT32_MAX ? (int)d : INT32_MAX;
+    wrow = wb + lane < p.rows;
+    wfull = ew > sw;
+  };
+  window(fetch(wb));
   int64_t open_rid = hrow;
   A open_val = R::id();
   __syncwarp();
   if (lo < hi) {
-    // chunk bases: positions whose address is 32-byte aligned
-    const int64_t q0 = lo - (int64_t)(((uintptr_t)(a + lo) & 31u) / sizeof(B));
     for (int64_t Bc = q0; Bc < hi; Bc += CH) {
       // valid positions of this chunk, relative to Bc: [rlo_c, rhi_c)
       const int rlo_c = (int)(lo > Bc ? lo - Bc : 0);
@@ -945,23 +954,22 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_vec(RaggedParams p)
         }
       }
       // rows starting in the chunk's valid range: flag their start position; empty ones are finished here
+      const int cb = (int)(Bc - q0);
       while (true) {
-        const int64_t r = wb + lane;
-        const int64_t d = sw - Bc;
-        const bool inr = r < p.rows && d >= rlo_c && d < rhi_c;
-        if (inr && ew > sw) {
-          const int rel = (int)d;
-          rid_map[(rel % EPL) * 32 + rel / EPL] = (int)(r - r0);
-          atomicOr(&flagw[rel / EPL], 1u << (rel % EPL));
+        const int d = wpos - cb;
+        const bool inr = wrow && d >= rlo_c && d < rhi_c;
+        if (inr && wfull) {
+          rid_map[(d % EPL) * 32 + d / EPL] = (int)(wb + lane - r0);
+          atomicOr(&flagw[d / EPL], 1u << (d % EPL));
         }
-        if (inr && ew == sw) finish(r, R::id());
-        const bool done = r >= p.rows || d < rhi_c;
+        if (inr && !wfull) finish(wb + lane, R::id());
+        const bool done = !wrow || d < rhi_c;
         if (__all_sync(FULL, done) && wb + 32 < p.rows) {
           wb += 32;
-          sw = nx;
+          const int64_t sw = nx;
           nx = nx2;
           nx2 = fetch(wb + 64);
-          ew = ends(sw, nx);
+          window(sw);
           continue;
         }
         break;
