@@ -509,7 +509,7 @@ struct Params2D {
   int64_t rows, cols, row_stride;
 };
 template <class R, int BLOCK, int U>
-__global__ void __launch_bounds__(BLOCK) k_2d(Params2D q) {
+__global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_2d(Params2D q) {
   using B = typename R::B;
   using A = typename R::A;
   using VT = typename Vec<B>::T;
@@ -524,11 +524,13 @@ __global__ void __launch_bounds__(BLOCK) k_2d(Params2D q) {
   const int64_t maxv = q.cols / VW;
   const int64_t per_row = maxv > 0 ? (maxv + CHV - 1) / CHV : 1;
   const int64_t items = q.rows * per_row;
+  // item it = (row r, chunk c), it = r * per_row + c, stepped by nw without a division per item
+  const int64_t dr = nw / per_row, dc = nw - dr * per_row;
+  int64_t r = gw / per_row, c = gw - r * per_row;
   A acc[VW];
 #pragma unroll
   for (int k = 0; k < VW; ++k) acc[k] = R::id();
   for (int64_t it = gw; it < items; it += nw) {
-    const int64_t r = it / per_row, c = it - r * per_row;
     const B* a = (const B*)q.f.a + r * q.row_stride;
     int64_t head = (int64_t)(((32u - ((uintptr_t)a & 31u)) & 31u) / sizeof(B));
     if (head > q.cols) head = q.cols;
@@ -554,6 +556,12 @@ __global__ void __launch_bounds__(BLOCK) k_2d(Params2D q) {
     if (c == 0) {
       if (lane < head) acc[0] = R::op(acc[0], R::lift(lds(a + lane)));
       if (lane < q.cols - tail0) acc[VW - 1] = R::op(acc[VW - 1], R::lift(lds(a + tail0 + lane)));
+    }
+    r += dr;
+    c += dc;
+    if (c >= per_row) {
+      c -= per_row;
+      ++r;
     }
   }
 #pragma unroll

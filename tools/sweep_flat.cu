@@ -167,6 +167,24 @@ void run_flat_tma(const char* name, void* buf, size_t bytes, void* ws, int sms) 
   printf("tmaflat %-7s S=%2d CHB=%6d NT=%d cps=%d W=%d  %7.3f ms  %7.1f GB/s\n", name, S, CHB, NT, CPS, WAIT, ms, bytes / ms / 1e6);
 }
 
+
+template <class R, int U>
+void run_2d(const char* name, void* buf, void* ws, int sms, int64_t rows, int64_t cols, int64_t stride, int cps) {
+  using B = typename R::B;
+  Params2D q{};
+  q.f.a = buf; q.f.mode = MODE_RESULT; q.f.out = (char*)ws + 4096; q.f.partials = (uint64_t*)((char*)ws + 8192);
+  q.f.tickets = (unsigned*)ws; q.f.world = 1;
+  q.rows = rows; q.cols = cols; q.row_stride = stride;
+  const int grid = sms * cps;
+  float ms = time_ms([&] { k_2d<R, 256, U><<<grid, 256>>>(q); }, 20);
+  CK(cudaGetLastError());
+  B res;
+  CK(cudaMemcpy(&res, q.f.out, sizeof(B), cudaMemcpyDeviceToHost));
+  const double bytes = (double)rows * cols * sizeof(B);
+  printf("2d %-6s %lldx%lld stride %lld U=%d cps=%d  %7.3f ms  %7.1f GB/s  result=%.17g\n", name,
+         (long long)rows, (long long)cols, (long long)stride, U, cps, ms, bytes / ms / 1e6, (double)res);
+}
+
 int main(int argc, char** argv) {
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
@@ -203,6 +221,19 @@ int main(int argc, char** argv) {
       run_flat<Red<IPM_ADD, IPM_F64>, 256, 8, 0>("f64+", buf, bytes, ws, sms);
       run_flat<Red<IPM_MAX, IPM_F64>, 256, 4, 0>("f64max", buf, bytes, ws, sms);
     }
+  }
+  if (mode == "2d") {
+    for (int shape = 0; shape < 3; ++shape) {
+      const int64_t rows = shape == 0 ? 16384 : shape == 1 ? 262144 : 4096, cols = shape == 0 ? 16000 : shape == 1 ? 1000 : 65000,
+                    stride = shape == 0 ? 16384 : shape == 1 ? 1024 : 65536;
+      for (int cps : {2, 4, 8}) {
+        run_2d<Red<IPM_ADD, IPM_F32>, 4>("f32+", buf, ws, sms, rows, cols, stride, cps);
+        run_2d<Red<IPM_ADD, IPM_F32>, 8>("f32+", buf, ws, sms, rows, cols, stride, cps);
+        run_2d<Red<IPM_ADD, IPM_F64>, 4>("f64+", buf, ws, sms, rows / 2, cols, stride, cps);
+        run_2d<Red<IPM_BXOR, IPM_I32>, 4>("i32^", buf, ws, sms, rows, cols, stride, cps);
+      }
+    }
+    return 0;
   }
   if (mode == "all" || mode == "seg") {
     printf("== segmented 65536 x 4096 f32\n");
