@@ -4,8 +4,10 @@
     torchrun --nproc-per-node N bench.py --gpus N ...        (one process per GPU, NCCL)
 
 One step = one execution of the clause over the whole 2^34-element iteration space: every rank runs the flat
-reduction kernel over its contiguous shard (rows a1-a6 of SURVEY.md §8(a)), one ncclAllGather exchanges the
-accumulator partials and a one-warp kernel folds them in rank order (a9), result left in device memory.
+reduction kernel over its contiguous shard (rows a1-a6 of SURVEY.md §8(a)); the kernel's last CTA exchanges the
+8-byte accumulator partials with the other ranks over NVLink peer memory and folds them in rank order (a9), result
+left in device memory — one launch per rank per step (fallback if peer mapping fails: ncclAllGather + a one-warp
+fold kernel).
 Inputs are generated on the device (ipmgen) before timing and are larger than L2 (64/N GiB per GPU), so no
 flush is needed between steps. Timed with CUDA events between two barriers, max over ranks.
 
@@ -13,7 +15,8 @@ Rank 0 prints ONE JSON line. Besides the contract keys it carries:
   roofline      the flat kernel's HBM roofline: algorithmic bytes per launch / its live per-launch event time
   cpu_baseline  the CPU oracle (test infrastructure, tests/ + here only) timed on a bounded sample, 1 core
   e2e           the same metric through ipm_reduce_host_dist: pinned host shards -> devices + the rank exchange
-  suite         (N=1) the other BASELINE configs device-timed: C1 latency, C2 per op, C3 segmented, C4 per op
+  suite         (N=1) the other BASELINE configs device-timed: C1 latency, C2 per op, C3 segmented, C4 per op,
+                the NEXT rows (fused, 2-D, ragged), and torch / CUB reductions on the same shapes as context
 `--impl reference` times the CPU oracle as the reference arm on the same metric (no GPU work).
 """
 from __future__ import annotations
@@ -22,6 +25,7 @@ import argparse
 import json
 import os
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -262,6 +266,16 @@ def suite(ipm, torch, ipmgen, peak):
             ctx[f"{name}_{dt}_2^{n.bit_length() - 1}"] = {"ms": ms, "GB/s": n * x.element_size() / ms / 1e6}
         del x
     out["library_context_torch"] = ctx
+    # and CUB's DeviceReduce (tools/cub_context.cu, a separate process; skipped if it was not built)
+    cub = os.path.join(os.path.dirname(os.path.abspath(__file__)), "tools", "bin", "cub_context")
+    if os.path.exists(cub):
+        torch.cuda.synchronize()
+        try:
+            r = subprocess.run([cub], capture_output=True, text=True, timeout=180)
+            out["library_context_cub"] = {d["case"]: {"ms": d["ms"], "GB/s": d["GB/s"]}
+                                          for d in (json.loads(l) for l in r.stdout.splitlines() if l.startswith("{"))}
+        except (subprocess.TimeoutExpired, ValueError) as e:
+            out["library_context_cub"] = {"error": str(e)[:200]}
 
     # NEXT rows: several variables in one pass (SRAD statistics, dot) and a strided 2-D region
     n = 1 << 28

@@ -80,10 +80,24 @@ def build_ipm(force: bool = False, extra: list[str] | None = None) -> str:
     return out
 
 
+def build_tools(force: bool = False) -> None:
+    """Library-context timing program (CUB DeviceReduce) that bench.py's suite runs if present. Optional: a
+    failure here does not fail the build."""
+    out = os.path.join(ROOT, "tools", "bin", "cub_context")
+    src = os.path.join(ROOT, "tools", "cub_context.cu")
+    if force or _stale(out, [src]):
+        os.makedirs(os.path.dirname(out), exist_ok=True)
+        try:
+            _run([NVCC, *ARCH, "-O3", "-std=c++17", "-o", out, src])
+        except RuntimeError as e:
+            sys.stderr.write(f"optional tool not built: {e}\n")
+
+
 def build_all(force: bool = False) -> None:
     build_oracle(force)
     build_gen(force)
     build_ipm(force)
+    build_tools(force)
 
 
 if __name__ == "__main__":
