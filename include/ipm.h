@@ -238,11 +238,14 @@ ipm_status ipm_flat_geometry(ipm_dtype dt, int64_t n, int* grid, int* block);
 /* ------------------------------------------------------------------ multi-GPU (one process per GPU)
  * The iteration space is sharded contiguously: rank r owns [r*n/P, (r+1)*n/P) (floor division, 128-bit
  * intermediate) — ipm_shard_range computes it (pure host function). Each rank reduces its shard on its GPU
- * into an accumulator-typed partial (no host sync), ONE ncclAllGather exchanges the P partials over
- * NVLink/NVSwitch, and every rank folds them in rank order, merges init and rounds — so every rank gets
- * the same bits, independent of NCCL's reduction order.
- * Bootstrap: rank 0 calls ipm_comm_unique_id, the id (ipm_comm_id_bytes() bytes) is broadcast out of band
- * (the Python binding uses the torch.distributed store), then every rank calls ipm_comm_init. */
+ * into an accumulator-typed partial (no host sync); the P partials are exchanged and every rank folds them in
+ * rank order, merges init and rounds — so every rank gets the same bits. Exchange:
+ * fused (default when every peer's 8 KiB symmetric slot buffer is mapped through CUDA IPC): the reduction
+ * kernel's last CTA stores the partial into every peer's buffer over NVLink and folds the P slots — one kernel
+ * per rank per call; otherwise ONE ncclAllGather of the partials + a one-warp fold kernel.
+ * Bootstrap with NCCL: rank 0 calls ipm_comm_unique_id, the id (ipm_comm_id_bytes() bytes) is broadcast out
+ * of band (the Python binding uses the torch.distributed store), then every rank calls ipm_comm_init (which
+ * also exchanges the slot-buffer IPC handles with ncclAllGather and agrees on the fused path). */
 typedef struct ipm_comm ipm_comm;
 size_t ipm_comm_id_bytes(void);
 ipm_status ipm_comm_unique_id(void* id_out);
@@ -252,6 +255,16 @@ ipm_status ipm_comm_destroy(ipm_comm* comm);
  * with the fused path only (no NCCL). Each rank's calls go on its own stream with its own workspace; the ranks'
  * kernels then run concurrently on the device. Used to exercise the multi-rank exchange on a single GPU. */
 ipm_status ipm_comm_init_group(ipm_comm** comms, int world, int device);
+/* Bootstrap WITHOUT NCCL (fused exchange only): every rank calls ipm_comm_create_ipc, which allocates its
+ * symmetric slot buffer and writes its CUDA IPC handle (ipm_comm_ipc_handle_bytes() bytes) to handle_out; the
+ * caller moves the handles between the ranks out of band (any transport) and every rank calls
+ * ipm_comm_attach_ipc with all `world` handles in rank order (its own included, ignored). The ranks are
+ * processes on the GPUs of one node (peer mappings over NVLink) or on the same GPU. attach returns IPM_E_CUDA
+ * if a peer buffer cannot be mapped; the ranks must then all give up (there is no fallback without NCCL). Until
+ * attach succeeds, reduce calls on the communicator return IPM_E_ARG. */
+size_t ipm_comm_ipc_handle_bytes(void);
+ipm_status ipm_comm_create_ipc(ipm_comm** comm, int rank, int world, int device, void* handle_out);
+ipm_status ipm_comm_attach_ipc(ipm_comm* comm, const void* handles);
 ipm_status ipm_shard_range(int64_t n, int rank, int world, int64_t* lo, int64_t* hi);
 /* dev_shard: this rank's n_shard elements (device); inout: host scalar, the same init on every rank (in),
  * the global result (out). Blocks until *inout is written. */

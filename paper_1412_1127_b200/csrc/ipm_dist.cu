@@ -176,6 +176,74 @@ ipm_status ipm_comm_init_group(ipm_comm** comms, int world, int device) {
   return IPM_OK;
 }
 
+size_t ipm_comm_ipc_handle_bytes(void) { return sizeof(cudaIpcMemHandle_t); }
+
+ipm_status ipm_comm_create_ipc(ipm_comm** comm, int rank, int world, int device, void* handle_out) {
+  if (!comm || !handle_out) {
+    set_error("NULL pointer");
+    return IPM_E_NULL;
+  }
+  if (world < 1 || world > WS_MAX_RANKS || rank < 0 || rank >= world) {
+    set_error("rank/world out of range (world <= 64)");
+    return IPM_E_ARG;
+  }
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  ipm_comm* m = new ipm_comm();
+  m->nccl = nullptr;
+  m->rank = rank;
+  m->world = world;
+  m->device = device;
+  m->p2p = 0;  // until ipm_comm_attach_ipc
+  if ((e = cudaMalloc(&m->sym, SYM_BYTES)) != cudaSuccess || (e = cudaMemset(m->sym, 0, SYM_BYTES)) != cudaSuccess ||
+      (e = cudaIpcGetMemHandle((cudaIpcMemHandle_t*)handle_out, m->sym)) != cudaSuccess) {
+    ipm_comm_destroy(m);
+    return cuda_fail(e, "symmetric slot buffer");
+  }
+  *comm = m;
+  return IPM_OK;
+}
+
+ipm_status ipm_comm_attach_ipc(ipm_comm* comm, const void* handles) {
+  if (!comm || !handles) {
+    set_error("NULL pointer");
+    return IPM_E_NULL;
+  }
+  if (comm->p2p || comm->nccl) {
+    set_error("communicator is already connected");
+    return IPM_E_ARG;
+  }
+  cudaError_t e = cudaSetDevice(comm->device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  const size_t hb = sizeof(cudaIpcMemHandle_t);
+  uint64_t* ptrs[64] = {nullptr};
+  for (int q = 0; q < comm->world; ++q) {
+    if (q == comm->rank) {
+      ptrs[q] = comm->sym;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, (const char*)handles + hb * q, hb);
+    void* ptr = nullptr;
+    if ((e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess)) != cudaSuccess) {
+      cudaGetLastError();
+      for (int k = 0; k < q; ++k)
+        if (comm->opened[k]) {
+          cudaIpcCloseMemHandle(comm->opened[k]);
+          comm->opened[k] = nullptr;
+        }
+      return cuda_fail(e, "cudaIpcOpenMemHandle(peer slot buffer)");
+    }
+    comm->opened[q] = ptr;
+    ptrs[q] = (uint64_t*)ptr;
+  }
+  if ((e = cudaMalloc(&comm->peers_dev, sizeof(uint64_t*) * comm->world)) != cudaSuccess ||
+      (e = cudaMemcpy(comm->peers_dev, ptrs, sizeof(uint64_t*) * comm->world, cudaMemcpyHostToDevice)) != cudaSuccess)
+    return cuda_fail(e, "peers");
+  comm->p2p = 1;
+  return IPM_OK;
+}
+
 ipm_status ipm_comm_destroy(ipm_comm* comm) {
   if (!comm) return IPM_OK;
   cudaDeviceSynchronize();
@@ -227,6 +295,10 @@ ipm_status ipm_reduce_dist_async(ipm_comm* comm, ipm_op op, ipm_dtype dt, const 
   if (!ws || ((uintptr_t)ws & 255u)) {
     set_error("workspace must be a non-NULL, 256-byte aligned device buffer");
     return IPM_E_WORKSPACE;
+  }
+  if (!comm->p2p && !comm->nccl) {
+    set_error("communicator not connected (ipm_comm_attach_ipc not called)");
+    return IPM_E_ARG;
   }
   cudaStream_t st = (cudaStream_t)stream;
   if (comm->p2p && (dist_mode_option() == 0 || !comm->nccl)) {  // one kernel: reduction + exchange
@@ -282,6 +354,10 @@ ipm_status ipm_reduce_host_dist(ipm_comm* comm, ipm_op op, ipm_dtype dt, const v
   if (!ws || ((uintptr_t)ws & 255u)) {
     set_error("workspace must be a non-NULL, 256-byte aligned device buffer");
     return IPM_E_WORKSPACE;
+  }
+  if (!comm->p2p && !comm->nccl) {
+    set_error("communicator not connected (ipm_comm_attach_ipc not called)");
+    return IPM_E_ARG;
   }
   cudaStream_t st = (cudaStream_t)stream;
   if ((s = stream_host_partial(op, dt, host_shard, n_shard, ws, st))) return s;

@@ -78,6 +78,9 @@ def _load():
         "ipm_comm_init": ([ctypes.POINTER(vp), ci, ci, vp, ci], ci),
         "ipm_comm_destroy": ([vp], ci),
         "ipm_comm_init_group": ([vp, ci, ci], ci),
+        "ipm_comm_ipc_handle_bytes": ([], sz),
+        "ipm_comm_create_ipc": ([ctypes.POINTER(vp), ci, ci, ci, vp], ci),
+        "ipm_comm_attach_ipc": ([vp, vp], ci),
         "ipm_shard_range": ([i64, ci, ci, ctypes.POINTER(i64), ctypes.POINTER(i64)], ci),
         "ipm_comm_uses_peer_memory": ([vp], ci),
         "ipm_comm_error": ([vp, ctypes.POINTER(ci)], ci),
@@ -98,7 +101,8 @@ EXPORTED = ("ipm_status_str ipm_last_error_message ipm_op_legal ipm_dtype_size i
             "ipm_present_count ipm_workspace_bytes ipm_workspace_init ipm_reduce ipm_reduce_async "
             "ipm_reduce_segmented ipm_reduce_ragged ipm_reduce_partials ipm_finalize_partials ipm_reduce_2d ipm_reduce_2d_async ipm_fused_nvars ipm_reduce_fused ipm_reduce_fused_async ipm_reduce_host ipm_release_staging ipm_set_option ipm_profile_enable ipm_profile_read "
             "ipm_profile_disable ipm_flat_geometry ipm_comm_id_bytes "
-            "ipm_comm_unique_id ipm_comm_init ipm_comm_destroy ipm_comm_init_group ipm_shard_range ipm_comm_uses_peer_memory ipm_comm_error "
+            "ipm_comm_unique_id ipm_comm_init ipm_comm_destroy ipm_comm_init_group ipm_comm_ipc_handle_bytes "
+            "ipm_comm_create_ipc ipm_comm_attach_ipc ipm_shard_range ipm_comm_uses_peer_memory ipm_comm_error "
             "ipm_reduce_host_dist ipm_reduce_dist "
             "ipm_reduce_dist_async").split()
 
@@ -536,6 +540,31 @@ class Comm:
             c.rank, c.world, c.device = r, world, device
             out.append(c)
         return out
+
+    @classmethod
+    def ipc(cls, rank: int, world: int, device: int, store, key: str = "ipm_ipc") -> "Comm":
+        """Bootstrap WITHOUT NCCL (ipm_comm_create_ipc / ipm_comm_attach_ipc): the slot-buffer IPC handles travel
+        through `store` (any torch.distributed Store). Fused exchange only. Every rank learns whether every other
+        rank mapped all peers; if any failed, all raise."""
+        torch.cuda.set_device(device)
+        hb = lib.ipm_comm_ipc_handle_bytes()
+        mine = ctypes.create_string_buffer(hb)
+        c = cls.__new__(cls)
+        c._h = ctypes.c_void_p()
+        c.rank, c.world, c.device = rank, world, device
+        _check(lib.ipm_comm_create_ipc(ctypes.byref(c._h), rank, world, device, mine), "ipm_comm_create_ipc")
+        store.set(f"{key}/handle/{rank}", bytes(mine.raw))
+        allh = b"".join(store.get(f"{key}/handle/{q}") for q in range(world))
+        buf = ctypes.create_string_buffer(allh, hb * world)
+        code = lib.ipm_comm_attach_ipc(c._h, buf)
+        msg = lib.ipm_last_error_message().decode(errors="replace") if code else ""
+        store.set(f"{key}/ok/{rank}", b"1" if code == 0 else b"0")
+        oks = [store.get(f"{key}/ok/{q}") == b"1" for q in range(world)]
+        if not all(oks):
+            c.close()
+            raise IpmError(code or 10, "Comm.ipc", msg or f"ranks {[q for q, o in enumerate(oks) if not o]} "
+                                                          "could not map every peer")
+        return c
 
     def __init__(self, rank: int, world: int, device: int, store=None, key: str = "ipm_nccl_id"):
         nb = lib.ipm_comm_id_bytes()

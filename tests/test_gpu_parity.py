@@ -2,6 +2,7 @@
 inputs. Bit-exact for integer, bitwise, logical, max and min; |g - o| <= tol*|o| for float + and * with
 tol = 1e-5 (float32) / 1e-12 (float64) against the oracle's long double value (BASELINE.json north_star)."""
 import ctypes
+import os
 import time
 
 import numpy as np
@@ -477,6 +478,39 @@ def test_dist_fused_multirank_one_gpu(ipm, world):
             check(op, dt, vals[0], want_t, want_ld)
     for c in comms:
         c.close()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_dist_ipc_processes_one_gpu(ipm, world, tmp_path):
+    """world PROCESSES on one GPU bootstrapped without NCCL (ipm_comm_create_ipc / ipm_comm_attach_ipc: the slot
+    buffers' CUDA IPC handles travel through a FileStore): the cross-process peer mapping + fused exchange, device
+    and host shards, every rank's bits equal and equal to the oracle's answer."""
+    import json
+    import subprocess
+    import sys
+
+    import ipc_worker
+    store = str(tmp_path / "store")
+    worker = os.path.join(os.path.dirname(os.path.abspath(__file__)), "ipc_worker.py")
+    procs = [subprocess.Popen([sys.executable, worker, str(r), str(world), store], stdout=subprocess.PIPE,
+                              stderr=subprocess.PIPE, text=True) for r in range(world)]
+    outs = []
+    for p in procs:
+        out, err = p.communicate(timeout=300)
+        assert p.returncode == 0, err[-2000:]
+        outs.append([json.loads(l) for l in out.splitlines() if l.startswith("{")])
+    per_case = len(ipc_worker.CASES) * (len(ipc_worker.INITS) + 1)
+    assert all(len(o) == per_case for o in outs)
+    for i in range(per_case):
+        rows = [o[i] for o in outs]
+        assert len({r["bits"] for r in rows}) == 1, rows         # every rank the same bits
+        r0 = rows[0]
+        case = next(c for c in ipc_worker.CASES if c[0] == r0["op"] and c[1] == r0["dt"])
+        op, dt, kind, n = case
+        h = ipmgen.fill_host(ipmgen.Spec(dt, n, kind, seed=ipc_worker.SEED))
+        want_t, want_ld = oracle.reduce(op, h, init=NPT[dt](r0["init"]))
+        got = np.frombuffer(bytes.fromhex(r0["bits"]), dtype=dt)[0]
+        check(op, dt, got, want_t, want_ld)
 
 
 # --------------------------------------------------------------------------- options, data clauses, host path edges
