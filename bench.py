@@ -266,16 +266,6 @@ def suite(ipm, torch, ipmgen, peak):
             ctx[f"{name}_{dt}_2^{n.bit_length() - 1}"] = {"ms": ms, "GB/s": n * x.element_size() / ms / 1e6}
         del x
     out["library_context_torch"] = ctx
-    # and CUB's DeviceReduce (tools/cub_context.cu, a separate process; skipped if it was not built)
-    cub = os.path.join(os.path.dirname(os.path.abspath(__file__)), "tools", "bin", "cub_context")
-    if os.path.exists(cub):
-        torch.cuda.synchronize()
-        try:
-            r = subprocess.run([cub], capture_output=True, text=True, timeout=180)
-            out["library_context_cub"] = {d["case"]: {"ms": d["ms"], "GB/s": d["GB/s"]}
-                                          for d in (json.loads(l) for l in r.stdout.splitlines() if l.startswith("{"))}
-        except (subprocess.TimeoutExpired, ValueError) as e:
-            out["library_context_cub"] = {"error": str(e)[:200]}
 
     # NEXT rows: several variables in one pass (SRAD statistics, dot) and a strided 2-D region
     n = 1 << 28
@@ -315,6 +305,21 @@ def suite(ipm, torch, ipmgen, peak):
                                                "frac": nbytes / med / 1e6 / peak, "kernels_per_call": 2}
     del vals, offs, o
     torch.cuda.empty_cache()
+    # library context: CUB's DeviceReduce / DeviceSegmentedReduce on the same shapes, including this ragged graph
+    # (tools/cub_context.cu, a separate process; skipped if it was not built)
+    cub = os.path.join(ROOT, "tools", "bin", "cub_context")
+    if os.path.exists(cub):
+        import tempfile
+        torch.cuda.synchronize()
+        with tempfile.NamedTemporaryFile(suffix=".bin") as f:
+            off.astype(np.int64).tofile(f.name)
+            try:
+                r = subprocess.run([cub, f.name], capture_output=True, text=True, timeout=300)
+                out["library_context_cub"] = {
+                    d["case"]: {"ms": d["ms"], "GB/s": d["GB/s"]}
+                    for d in (json.loads(l) for l in r.stdout.splitlines() if l.startswith("{"))}
+            except (subprocess.TimeoutExpired, ValueError) as e:
+                out["library_context_cub"] = {"error": str(e)[:200]}
     return out
 
 
