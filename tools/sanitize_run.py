@@ -42,6 +42,18 @@ for dt in TD:
     for sig in ("sum_sumsq", "dot", "minmax", "stats"):
         ipm.reduce_fused(sig, x[1:2001], x[3:2003] if sig == "dot" else None)
     ipm.reduce_2d("max", x, rows=7, cols=300, row_stride=700)
+    # a power-law graph: short rows packed several per lane (shared-memory parked segments), rows split across
+    # warps (head/tail records + fix-up), empty rows
+    off2 = ipmgen.offsets_from_degrees(ipmgen.degrees(1 << 14, seed=4, mean=6.0))
+    z = torch.empty(int(off2[-1]) + 1, dtype=TD[dt], device="cuda")
+    ipmgen.fill_device(ipmgen.Spec(dt, z.numel(), "random", seed=4), z.data_ptr(), 0, z.numel(),
+                       torch.cuda.current_stream().cuda_stream)
+    ipm.reduce_ragged("max", z[1:], torch.from_numpy(off2).cuda())
+    for rows, cols, stride in [(33, 1000, 1024), (5, 4099, 4101), (200, 31, 37)]:
+        w = torch.empty(rows * stride + 1, dtype=TD[dt], device="cuda")
+        ipmgen.fill_device(ipmgen.Spec(dt, w.numel(), "random", seed=5), w.data_ptr(), 0, w.numel(),
+                           torch.cuda.current_stream().cuda_stream)
+        ipm.reduce_2d("+", w[1:], rows=rows, cols=cols, row_stride=stride)
 ipm.set_option("dist_timeout_ms", 3000)  # the sanitizer may serialise the two ranks' kernels
 comms = ipm.Comm.group(2)
 y = torch.arange(100_003, dtype=torch.float64, device="cuda")
