@@ -415,6 +415,44 @@ static ipm_status release_staging_locked() {
 using namespace ipm;
 
 // ============================================================================================ C ABI
+// Synchronous calls deliver the 8-byte result through a small pinned, device-mapped host buffer per host thread
+// and device: the finishing kernel stores the result straight into host memory, so the call is launch + stream
+// synchronize (no separate device-to-host copy through a pageable staging buffer). One per thread suffices: a
+// thread has at most one synchronous call in flight.
+namespace ipm {
+namespace {
+struct Mailbox {
+  void* host[64] = {nullptr};
+  void* dev[64] = {nullptr};
+};
+thread_local Mailbox tl_mail;
+}  // namespace
+
+ipm_status result_mailbox(void** host, void** dev) {
+  int d = 0;
+  CK(cudaGetDevice(&d));
+  if (d < 0 || d >= 64) {
+    set_error("device index out of range for the result mailbox");
+    return IPM_E_ARG;
+  }
+  if (!tl_mail.host[d]) {
+    void* h = nullptr;
+    CK(cudaHostAlloc(&h, 64, cudaHostAllocMapped | cudaHostAllocPortable));
+    void* dp = nullptr;
+    cudaError_t e = cudaHostGetDevicePointer(&dp, h, 0);
+    if (e != cudaSuccess) {
+      cudaFreeHost(h);
+      return cuda_fail(e, "cudaHostGetDevicePointer");
+    }
+    tl_mail.host[d] = h;
+    tl_mail.dev[d] = dp;
+  }
+  *host = tl_mail.host[d];
+  *dev = tl_mail.dev[d];
+  return IPM_OK;
+}
+}  // namespace ipm
+
 extern "C" {
 
 const char* ipm_status_str(ipm_status s) {
@@ -552,12 +590,12 @@ ipm_status ipm_reduce(ipm_op op, ipm_dtype dt, const void* dev, int64_t n, void*
     set_error("NULL inout");
     return IPM_E_NULL;
   }
-  void* res = (char*)ws + WS_RESULT;
-  ipm_status s = ipm_reduce_async(op, dt, dev, n, inout, res, ws, stream);
+  void *mh, *md;
+  ipm_status s = result_mailbox(&mh, &md);
   if (s) return s;
-  cudaStream_t st = (cudaStream_t)stream;
-  CK(cudaMemcpyAsync(inout, res, esize(dt), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));  // end of the compute region
+  if ((s = ipm_reduce_async(op, dt, dev, n, inout, md, ws, stream))) return s;
+  CK(cudaStreamSynchronize((cudaStream_t)stream));  // end of the compute region
+  memcpy(inout, mh, esize(dt));
   return IPM_OK;
 }
 
@@ -817,12 +855,12 @@ ipm_status ipm_reduce_2d(ipm_op op, ipm_dtype dt, const void* dev, int64_t rows,
     set_error("NULL inout");
     return IPM_E_NULL;
   }
-  void* res = (char*)ws + WS_RESULT;
-  ipm_status s = ipm_reduce_2d_async(op, dt, dev, rows, cols, row_stride, inout, res, ws, stream);
+  void *mh, *md;
+  ipm_status s = result_mailbox(&mh, &md);
   if (s) return s;
-  cudaStream_t st = (cudaStream_t)stream;
-  CK(cudaMemcpyAsync(inout, res, esize(dt), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
+  if ((s = ipm_reduce_2d_async(op, dt, dev, rows, cols, row_stride, inout, md, ws, stream))) return s;
+  CK(cudaStreamSynchronize((cudaStream_t)stream));
+  memcpy(inout, mh, esize(dt));
   return IPM_OK;
 }
 
@@ -879,12 +917,12 @@ ipm_status ipm_reduce_fused(ipm_fused f, ipm_dtype dt, const void* x, const void
     set_error("NULL inout");
     return IPM_E_NULL;
   }
-  void* res = (char*)ws + WS_RESULT;
-  ipm_status s = ipm_reduce_fused_async(f, dt, x, y, n, inout, res, ws, stream);
+  void *mh, *md;
+  ipm_status s = result_mailbox(&mh, &md);
   if (s) return s;
-  cudaStream_t st = (cudaStream_t)stream;
-  CK(cudaMemcpyAsync(inout, res, esize(dt) * fused_nvars(f), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
+  if ((s = ipm_reduce_fused_async(f, dt, x, y, n, inout, md, ws, stream))) return s;
+  CK(cudaStreamSynchronize((cudaStream_t)stream));
+  memcpy(inout, mh, esize(dt) * fused_nvars(f));  // <= 4 variables x 8 bytes
   return IPM_OK;
 }
 
@@ -961,12 +999,13 @@ ipm_status ipm_reduce_host(ipm_op op, ipm_dtype dt, const void* host, int64_t n,
     return IPM_E_NULL;
   }
   cudaStream_t st = (cudaStream_t)stream;
-  void* res = (char*)ws + WS_RESULT;
+  void *mh, *md;
+  if ((s = result_mailbox(&mh, &md))) return s;
   if ((s = stream_host_partial(op, dt, host, n, ws, st))) return s;
-  if ((s = launch_finalize(op, dt, (const uint64_t*)((char*)ws + WS_ACC), 1, scalar_bits(dt, inout), 1, res, st)))
+  if ((s = launch_finalize(op, dt, (const uint64_t*)((char*)ws + WS_ACC), 1, scalar_bits(dt, inout), 1, md, st)))
     return s;
-  CK(cudaMemcpyAsync(inout, res, esize(dt), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  memcpy(inout, mh, esize(dt));
   return IPM_OK;
 }
 

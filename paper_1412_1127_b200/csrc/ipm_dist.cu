@@ -321,13 +321,13 @@ ipm_status ipm_reduce_dist(ipm_comm* comm, ipm_op op, ipm_dtype dt, const void* 
     set_error("NULL inout");
     return IPM_E_NULL;
   }
-  void* res = (char*)ws + WS_RESULT;
-  ipm_status s = ipm_reduce_dist_async(comm, op, dt, dev_shard, n_shard, inout, res, ws, stream);
+  void *mh, *md;
+  ipm_status s = result_mailbox(&mh, &md);
   if (s) return s;
-  cudaStream_t st = (cudaStream_t)stream;
-  cudaError_t e = cudaMemcpyAsync(inout, res, esize(dt), cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if ((s = ipm_reduce_dist_async(comm, op, dt, dev_shard, n_shard, inout, md, ws, stream))) return s;
+  cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "ipm_reduce_dist");
+  memcpy(inout, mh, esize(dt));
   ncclResult_t ar;
   if (comm->nccl && ncclCommGetAsyncError(comm->nccl, &ar) == ncclSuccess && ar != ncclSuccess)
     return nccl_fail(ar, "ncclCommGetAsyncError");
@@ -362,7 +362,8 @@ ipm_status ipm_reduce_host_dist(ipm_comm* comm, ipm_op op, ipm_dtype dt, const v
   cudaStream_t st = (cudaStream_t)stream;
   if ((s = stream_host_partial(op, dt, host_shard, n_shard, ws, st))) return s;
   const uint64_t* acc = (const uint64_t*)((char*)ws + WS_ACC);
-  void* res = (char*)ws + WS_RESULT;
+  void *mh, *res;
+  if ((s = result_mailbox(&mh, &res))) return s;
   const uint64_t ib = scalar_bits(dt, inout);
   if (comm->p2p && (dist_mode_option() == 0 || !comm->nccl)) {
     DistArgs d{comm->peers_dev, comm->rank, comm->world, dist_timeout_ns()};
@@ -373,9 +374,9 @@ ipm_status ipm_reduce_host_dist(ipm_comm* comm, ipm_op op, ipm_dtype dt, const v
     if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather");
     if ((s = launch_finalize(op, dt, slots, comm->world, ib, 1, res, st))) return s;
   }
-  cudaError_t e = cudaMemcpyAsync(inout, res, esize(dt), cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaError_t e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "ipm_reduce_host_dist");
+  memcpy(inout, mh, esize(dt));
   int err = 0;
   if (comm->p2p && ipm_comm_error(comm, &err) == IPM_OK && err) {
     set_error("fused exchange: a peer did not arrive within the timeout (result undefined)");

@@ -27,6 +27,8 @@ void set_error(const std::string& msg);
 ipm_status cuda_fail(cudaError_t e, const char* where);
 
 int sm_count();  // of the current device (cached)
+// pinned, device-mapped 64-byte result buffer of the calling host thread on the current device
+ipm_status result_mailbox(void** host, void** dev);
 
 ipm_status validate(ipm_op op, ipm_dtype dt);
 size_t esize(ipm_dtype dt);
