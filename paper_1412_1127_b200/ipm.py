@@ -157,8 +157,15 @@ def legal(op: str, dtype) -> bool:
     return bool(lib.ipm_op_legal(op_code(op), dtype_code(dtype)))
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def _stream(stream=None) -> int:
     if stream is None:
+        # torch's current stream of the current device; the raw accessor avoids building a Stream object
+        # (~3 us per call, measured by tools/py_overhead.py)
+        if _raw_stream is not None:
+            return _raw_stream(torch.cuda.current_device())
         return torch.cuda.current_stream().cuda_stream
     return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
 
@@ -188,7 +195,7 @@ _ws_lock = threading.Lock()
 def workspace(stream=None, device=None) -> torch.Tensor:
     """The per-(device, stream) zero-initialised workspace used when none is passed explicitly."""
     dev = torch.cuda.current_device() if device is None else device
-    s = _stream(stream)
+    s = stream if isinstance(stream, int) else _stream(stream)
     with _ws_lock:
         ws = _ws_cache.get((dev, s))
         if ws is None:
@@ -214,12 +221,9 @@ def reduce(op: str, t: torch.Tensor, init=None, ws: torch.Tensor | None = None, 
         return reduce_2d(op, t, init=init, ws=ws, stream=stream)
     ptr, n, dt = _flat_arg(t)
     s = _stream(stream)
-    ws = workspace(stream) if ws is None else ws
-    box = _scalar(dt, init)
-    if box is None:  # no original value: start from the identity (the async path does that on device)
-        out = reduce_async(op, t, None, ws=ws, stream=stream)
-        _sync(stream)
-        return out.cpu().numpy()[0]
+    ws = workspace(s) if ws is None else ws
+    # no original value: start from the identity, which leaves the fold unchanged
+    box = _scalar(dt, identity_value(op, dt) if init is None else init)
     _check(lib.ipm_reduce(op_code(op), dt, ptr, n, box.ctypes.data, ws.data_ptr(), s), "ipm_reduce")
     return box[0]
 
@@ -322,14 +326,12 @@ def reduce_2d(op: str, t: torch.Tensor, rows: int | None = None, cols: int | Non
     elif rows is None or cols is None:
         raise ValueError("rows and cols are required for a flat tensor")
     row_stride = cols if row_stride is None else row_stride
-    ws = workspace(stream) if ws is None else ws
-    out = torch.empty(1, dtype=t.dtype, device=t.device)
-    box = _scalar(dt, init)
-    _check(lib.ipm_reduce_2d_async(op_code(op), dt, t.data_ptr(), rows, cols, row_stride,
-                                   None if box is None else box.ctypes.data, out.data_ptr(), ws.data_ptr(),
-                                   _stream(stream)), "ipm_reduce_2d_async")
-    _sync(stream)
-    return out.cpu().numpy()[0]
+    s = _stream(stream)
+    ws = workspace(s) if ws is None else ws
+    box = _scalar(dt, identity_value(op, dt) if init is None else init)
+    _check(lib.ipm_reduce_2d(op_code(op), dt, t.data_ptr(), rows, cols, row_stride, box.ctypes.data, ws.data_ptr(), s),
+           "ipm_reduce_2d")
+    return box[0]
 
 
 FUSED = {"sum_sumsq": 0, "dot": 1, "minmax": 2, "stats": 3}
@@ -396,9 +398,16 @@ def reduce_host(op: str, a, init=None, ws: torch.Tensor | None = None, stream=No
 
 
 def identity_value(op: str, dt: int):
-    """The identity of op on element type dt, as the library's own finalize kernel produces it (n = 0)."""
-    out = reduce_async(op, torch.empty(0, dtype=TORCH_OF[dt], device="cuda"))
-    return out.cpu().numpy()[0]
+    """The identity of op on element type dt (SURVEY.md §8(c) identity column: 0, 1, the type's minimum /
+    maximum (-inf / +inf for floats), all ones, 0, 0, 1, 0). tests/test_gpu_parity.py checks that it equals what
+    the library's own finalize kernel returns for n = 0."""
+    op_code(op)  # unknown operator -> ValueError
+    np_t = np.dtype(NP_OF[dt])
+    if np_t.kind == "f":
+        lo, hi = -np.inf, np.inf
+    else:
+        lo, hi = np.iinfo(np_t).min, np.iinfo(np_t).max
+    return np_t.type({"+": 0, "*": 1, "max": lo, "min": hi, "&": -1, "|": 0, "^": 0, "&&": 1, "||": 0}[op])
 
 
 OPTIONS = {"flat_ctas_per_sm": 0, "seg_kernel": 1, "deterministic": 2, "dist_mode": 3, "dist_timeout_ms": 4}
@@ -605,11 +614,7 @@ class Comm:
         """Every rank passes its shard and the same init; every rank returns the global result."""
         ptr, n, dt = _flat_arg(shard)
         ws = workspace(stream) if ws is None else ws
-        box = _scalar(dt, init)
-        if box is None:
-            out = self.reduce_async(op, shard, None, ws=ws, stream=stream)
-            _sync(stream)
-            return out.cpu().numpy()[0]
+        box = _scalar(dt, identity_value(op, dt) if init is None else init)
         _check(lib.ipm_reduce_dist(self._h, op_code(op), dt, ptr, n, box.ctypes.data, ws.data_ptr(),
                                    _stream(stream)), "ipm_reduce_dist")
         return box[0]

@@ -110,9 +110,12 @@ def test_flat_no_init_is_identity_start(ipm, op, dt):
     got = ipm.reduce(op, x)
     want_t, want_ld = oracle.reduce(op, ipmgen.fill_host(spec))
     check(op, dt, got, want_t, want_ld)
-    # the identity itself (n = 0, no init)
-    e = ipm.reduce(op, x[:0])
-    assert bits(e, dt) == bits(oracle.identity(op, dt), dt)
+    # the identity itself (n = 0, no init): the library's finalize kernel, the synchronous call (which starts
+    # from the binding's host-side identity table) and that table all agree with the oracle
+    want = bits(oracle.identity(op, dt), dt)
+    assert bits(ipm.reduce_async(op, x[:0]).cpu().numpy()[0], dt) == want
+    assert bits(ipm.reduce(op, x[:0]), dt) == want
+    assert bits(ipm.identity_value(op, ipm.dtype_code(TD[dt])), dt) == want
 
 
 @pytest.mark.parametrize("dt", DTS)
