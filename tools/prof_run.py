@@ -19,13 +19,14 @@ TD = {"int32": torch.int32, "int64": torch.int64, "float32": torch.float32, "flo
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5", "stats", "dot", "2d"])
     ap.add_argument("--op", default="+")
     ap.add_argument("--dtype", default="float32")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--log2n", type=int, default=None)
     a = ap.parse_args()
-    n = {"c1": 1 << 20, "c2": 1 << 28, "c3": 65536 * 4096, "c4": 1 << 30, "c5": 1 << 34}[a.config]
+    n = {"c1": 1 << 20, "c2": 1 << 28, "c3": 65536 * 4096, "c4": 1 << 30, "c5": 1 << 34, "stats": 1 << 28,
+         "dot": 1 << 29, "2d": 16384 * 16384}[a.config]
     if a.log2n:
         n = 1 << a.log2n
     kind = {"+": "random", "*": "signs", "max": "signed", "min": "signed", "&": "allbits", "|": "random",
@@ -37,6 +38,12 @@ def main():
     for _ in range(a.reps):
         if a.config == "c3":
             ipm.reduce_segmented(a.op, x.view(65536, 4096))
+        elif a.config == "stats":  # the suite's fused row: [sum, sum of squares, min, max] in one pass
+            ipm.reduce_fused_async("stats", x)
+        elif a.config == "dot":    # two streams of 2^28
+            ipm.reduce_fused_async("dot", x[: 1 << 28], x[1 << 28:])
+        elif a.config == "2d":     # a 16384 x 16000 window of a 16384 x 16384 image
+            ipm.reduce_2d(a.op, x.view(16384, 16384)[:, :16000])
         else:
             ipm.reduce_async(a.op, x)
     torch.cuda.synchronize()
