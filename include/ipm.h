@@ -202,11 +202,12 @@ ipm_status ipm_reduce_host(ipm_op op, ipm_dtype dt, const void* host, int64_t n,
 ipm_status ipm_release_staging(void);
 
 /* Kernel timing (tracing): while enabled, the library records a CUDA event pair on the launch stream around
- * each reduction kernel it launches (flat, segmented; not the one-warp finalize), up to max_records launches
- * (later launches are not recorded). ipm_profile_read waits for the recorded events and returns the
- * per-launch durations in milliseconds, in launch order, plus the number of recorded launches; it also
- * returns the kernel kind of each record in `kinds` (0 flat, 1 segmented) when non-NULL. Disable frees the
- * events. Not thread-safe with concurrent launches from other threads. */
+ * each reduction kernel it launches (not the one-warp finalize), up to max_records launches (later launches
+ * are not recorded). ipm_profile_read waits for the recorded events and returns the per-launch durations in
+ * milliseconds, in launch order, plus the number of recorded launches; it also returns the kernel kind of each
+ * record in `kinds` when non-NULL: 0 flat (incl. per-block partials and the fused multi-GPU exchange),
+ * 1 segmented, 2 several variables (fused), 3 strided 2-D, 4 ragged (one record covers the ragged kernel and
+ * its fix-up). Disable frees the events. Not thread-safe with concurrent launches from other threads. */
 ipm_status ipm_profile_enable(int max_records);
 ipm_status ipm_profile_read(float* ms, int* kinds, int max, int* count);
 ipm_status ipm_profile_disable(void);

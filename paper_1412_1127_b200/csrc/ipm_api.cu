@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -53,13 +54,15 @@ constexpr int FLAT_BLOCK = 256;
 constexpr int FLAT_U = 4;    // static / dynamic k_flat: 4 x 32 B loads per thread per tile
 constexpr int GUIDED_U = 2;  // k_flat_guided: 2 x 32 B per tile, software-pipelined (2-4 loads in flight)
 // run-time options (ipm_set_option); defaults chosen by tools/sweep_flat.cu measurements
-static int g_opt_flat_cps = -1;  // CTAs per SM for k_flat (-1: IPM_CTAS_PER_SM env or 4)
-static int g_opt_seg_kernel = 0; // 0 auto (= 1), 1 warp per row (direct loads), 2 warp per row (TMA ring)
-static int g_opt_deterministic = 1;  // 1: guided deterministic schedule for the flat kernel
-static int g_opt_dist_mode = 0;      // 0: fused peer-memory exchange when mapped, 1: NCCL AllGather
-static long long g_opt_dist_timeout_ms = 30000;
+// process-wide, set from any thread: atomics (a launch reads each once)
+static std::atomic<int> g_opt_flat_cps{-1};  // CTAs per SM for k_flat (-1: IPM_CTAS_PER_SM env or 4)
+static std::atomic<int> g_opt_seg_kernel{0}; // 0 auto (= 1), 1 warp per row (direct loads), 2 warp per row (TMA ring)
+static std::atomic<int> g_opt_deterministic{1};  // 1: guided deterministic schedule for the flat kernel
+static std::atomic<int> g_opt_dist_mode{0};      // 0: fused peer-memory exchange when mapped, 1: NCCL AllGather
+static std::atomic<long long> g_opt_dist_timeout_ms{30000};
 static int flat_ctas_per_sm() {
-  if (g_opt_flat_cps > 0) return g_opt_flat_cps;
+  const int c = g_opt_flat_cps.load(std::memory_order_relaxed);
+  if (c > 0) return c;
   static int v = std::max(1, std::min(8, env_int("IPM_CTAS_PER_SM", 4)));
   return v;
 }
@@ -141,8 +144,8 @@ static void prof_free() {
   g_prof = Prof();
 }
 
-int dist_mode_option() { return g_opt_dist_mode; }
-long long dist_timeout_ns() { return g_opt_dist_timeout_ms * 1000000ll; }
+int dist_mode_option() { return g_opt_dist_mode.load(std::memory_order_relaxed); }
+long long dist_timeout_ns() { return g_opt_dist_timeout_ms.load(std::memory_order_relaxed) * 1000000ll; }
 
 // ------------------------------------------------------------------------------------------ dispatch
 #define IPM_LEGAL(X)                                                                                       \
@@ -166,8 +169,9 @@ struct Launch {
   static void flat(const FlatParams& p, dim3 grid, cudaStream_t st) {
     // up to 64 MiB the launch is latency-bound: the static schedule saves the chunk claims (C1: 12.4 -> 10.3 us)
     const bool small = p.n * (int64_t)sizeof(typename R::B) <= (64ll << 20);
-    if (p.counter && grid.y == 1 && grid.x > 1 && g_opt_deterministic != 2 && !small) {
-      if (g_opt_deterministic) k_flat_guided<R, FLAT_BLOCK, GUIDED_U, true><<<grid, FLAT_BLOCK, 0, st>>>(p);
+    const int det = g_opt_deterministic.load(std::memory_order_relaxed);
+    if (p.counter && grid.y == 1 && grid.x > 1 && det != 2 && !small) {
+      if (det) k_flat_guided<R, FLAT_BLOCK, GUIDED_U, true><<<grid, FLAT_BLOCK, 0, st>>>(p);
       else k_flat<R, FLAT_BLOCK, FLAT_U, 0, 2><<<grid, FLAT_BLOCK, 0, st>>>(p);
     } else {
       k_flat<R, FLAT_BLOCK, FLAT_U, 0, 0><<<grid, FLAT_BLOCK, 0, st>>>(p);
@@ -669,7 +673,7 @@ ipm_status ipm_reduce_segmented(ipm_op op, ipm_dtype dt, const void* dev, int64_
   p.has_init = has_init;
   p.out = dev_out;
   ProfScope ps(st, 1);
-  const bool tma = g_opt_seg_kernel == 2 && cols * (int64_t)esize(dt) >= 64;
+  const bool tma = g_opt_seg_kernel.load(std::memory_order_relaxed) == 2 && cols * (int64_t)esize(dt) >= 64;
   if (tma) {         // one warp per row, rows staged by TMA bulk copies (one 128 KiB-ring CTA per SM)
     const int64_t blocks = std::min<int64_t>((rows + TMA_WARPS - 1) / TMA_WARPS, (int64_t)sms);
     CK(t->seg_tma(p, (int)std::max<int64_t>(1, blocks), st));
