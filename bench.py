@@ -458,8 +458,8 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.empty_cache()
 
     if rank == 0:
-        cpu = None
-        if not args.no_cpu:
+        cpu = None  # the oracle baseline runs at N = 1 only (a bounded host sample; the same at any N)
+        if not args.no_cpu and world == 1:
             xs = torch.empty(min(n_shard, 1 << 30), dtype=torch.float32, device="cuda")
             ipmgen.fill_device(spec, xs.data_ptr(), lo, xs.numel(), torch.cuda.current_stream().cuda_stream)
             cpu = cpu_baseline_oracle(xs)
