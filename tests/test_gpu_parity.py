@@ -402,6 +402,12 @@ def ragged_cases():
     yield "powerlaw", ipmgen.offsets_from_degrees(ipmgen.degrees(20_000, seed=3))
     d = np.zeros(300, np.int64); d[[0, 150, 299]] = [100_000, 1_000_000, 7]
     yield "huge_rows", ipmgen.offsets_from_degrees(d)
+    # > 512 elements per warp at 148 x 32 warps: whole chunks in which no row starts (the flag-free path),
+    # long rows next to runs of short and empty ones, empty rows after the last element
+    d = ipmgen.degrees(1500, kind="const", mean=4096)
+    d[100:400] = np.arange(300) % 5
+    d[-3:] = 0
+    yield "long_rows", ipmgen.offsets_from_degrees(d, 1)
 
 
 @pytest.mark.parametrize("op,dt", LEGAL)
