@@ -49,6 +49,12 @@ for dt in TD:
     ipmgen.fill_device(ipmgen.Spec(dt, z.numel(), "random", seed=4), z.data_ptr(), 0, z.numel(),
                        torch.cuda.current_stream().cuda_stream)
     ipm.reduce_ragged("max", z[1:], torch.from_numpy(off2).cuda())
+    # > 512 elements per warp: whole chunks in which no row starts (the flag-free path), rows across many warps
+    off3 = np.array([0, 1_500_000, 1_500_003, 3_000_000, 3_000_000, 3_000_017, 4_600_000], np.int64) + 1
+    z = torch.empty(int(off3[-1]) + 2, dtype=TD[dt], device="cuda")
+    ipmgen.fill_device(ipmgen.Spec(dt, z.numel(), "random", seed=6), z.data_ptr(), 0, z.numel(),
+                       torch.cuda.current_stream().cuda_stream)
+    ipm.reduce_ragged("+", z, torch.from_numpy(off3).cuda())
     for rows, cols, stride in [(33, 1000, 1024), (5, 4099, 4101), (200, 31, 37)]:
         w = torch.empty(rows * stride + 1, dtype=TD[dt], device="cuda")
         ipmgen.fill_device(ipmgen.Spec(dt, w.numel(), "random", seed=5), w.data_ptr(), 0, w.numel(),
