@@ -182,11 +182,14 @@ struct Launch {
   }
   static void ragged(const RaggedParams& p, int blocks, int64_t nw, cudaStream_t st) {
     // 25 KiB of static shared memory per CTA: ask for the largest carveout so 8 CTAs fit on an SM
-    static const bool carveout = cudaFuncSetAttribute(k_ragged_vec<R, 4, 8, 2>,
+    // L2 prefetch of the next chunk (profiles/r01_sweep_ragged_5_l2prefetch.txt: +13-16 % on long rows, +1-7 % on
+    // the power-law graph); for the widened float32 + * fold (issue-bound on short rows) only inside long rows
+    constexpr int PFV = sizeof(typename R::A) > sizeof(typename R::B) ? -1 : 1;
+    static const bool carveout = cudaFuncSetAttribute(k_ragged_vec<R, 4, 8, 2, true, PFV>,
                                                       cudaFuncAttributePreferredSharedMemoryCarveout,
                                                       (int)cudaSharedmemCarveoutMaxShared) == cudaSuccess;
     (void)carveout;
-    k_ragged_vec<R, 4, 8, 2><<<blocks, 128, 0, st>>>(p);  // 8 CTAs x 4 warps per SM, 2 vectors per lane
+    k_ragged_vec<R, 4, 8, 2, true, PFV><<<blocks, 128, 0, st>>>(p);  // 8 CTAs x 4 warps per SM, 2 vectors per lane
     k_ragged_fix<R><<<(unsigned)((nw + 7) / 8), 256, 0, st>>>(p, nw);
   }
   static void two_d(const Params2D& q, int grid, cudaStream_t st) {

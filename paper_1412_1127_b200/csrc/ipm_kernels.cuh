@@ -499,6 +499,18 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_flat_guided(FlatParams 
   }
 }
 
+// L2 prefetch of a byte range (one bulk-prefetch instruction; only the 16-byte-aligned interior is named, so
+// nothing outside [p, p + bytes) is touched). Issued by one lane for data the warp reads next.
+__device__ __forceinline__ void l2_prefetch(const void* p, int64_t bytes) {
+  const uintptr_t b0 = ((uintptr_t)p + 15u) & ~(uintptr_t)15u;
+  const uintptr_t b1 = ((uintptr_t)p + (uintptr_t)bytes) & ~(uintptr_t)15u;
+  if (bytes > 0 && b1 > b0) {
+    const uint64_t nb = b1 - b0;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(b0), "r"((uint32_t)(nb < 0xFFFFFFF0ull ? nb : 0xFFFFFFF0ull))
+                 : "memory");
+  }
+}
+
 // ------------------------------------------------------------------------------------------ 2-D collapse
 // One scalar over a strided 2-D region (a gang loop over rows collapsed with the
 // vector loop over columns, rows not contiguous when row_stride > cols): work items are (row, chunk of
@@ -508,7 +520,7 @@ struct Params2D {
   FlatParams f;   // f.a = base, f.n unused
   int64_t rows, cols, row_stride;
 };
-template <class R, int BLOCK, int U>
+template <class R, int BLOCK, int U, int PF = 0>
 __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_2d(Params2D q) {
   using B = typename R::B;
   using A = typename R::A;
@@ -531,6 +543,15 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_2d(Params2D q) {
 #pragma unroll
   for (int k = 0; k < VW; ++k) acc[k] = R::id();
   for (int64_t it = gw; it < items; it += nw) {
+    if (PF && lane == 0 && it + nw < items) {  // the warp's next item (row, chunk) into L2
+      int64_t rn = r + dr, cn = c + dc;
+      if (cn >= per_row) {
+        cn -= per_row;
+        ++rn;
+      }
+      const int64_t e0 = cn * CHV * VW, e1 = e0 + CHV * VW + VW;
+      l2_prefetch((const B*)q.f.a + rn * q.row_stride + e0, ((e1 < q.cols ? e1 : q.cols) - e0) * (int64_t)sizeof(B));
+    }
     const B* a = (const B*)q.f.a + r * q.row_stride;
     int64_t head = (int64_t)(((32u - ((uintptr_t)a & 31u)) & 31u) / sizeof(B));
     if (head > q.cols) head = q.cols;
@@ -582,7 +603,7 @@ struct SegParams {
 };
 
 // one warp per row (gang = the grid of warps over rows, vector = the 32 lanes over the row's columns)
-template <class R, int WARPS, int U, int HINT = 0>
+template <class R, int WARPS, int U, int HINT = 0, int PF = 0>
 __global__ void __launch_bounds__(WARPS * 32) k_seg_warp(SegParams p) {
   using B = typename R::B;
   using A = typename R::A;
@@ -592,6 +613,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_seg_warp(SegParams p) {
   const int64_t gw = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5);
   const int64_t nw = (int64_t)gridDim.x * WARPS;
   for (int64_t r = gw; r < p.rows; r += nw) {
+    if (PF && lane == 0 && r + nw < p.rows)  // the warp's next row into L2
+      l2_prefetch((const B*)p.a + (r + nw) * p.row_stride, p.cols * (int64_t)sizeof(B));
     const B* a = (const B*)p.a + r * p.row_stride;
     const int64_t n = p.cols;
     int64_t head = (int64_t)(((32u - ((uintptr_t)a & 31u)) & 31u) / sizeof(B));
@@ -872,7 +895,7 @@ __device__ __forceinline__ A shfl_acc(A v, int src) {
   return unpack<A>(__shfl_sync(FULL, pack(v), src));
 }
 
-template <class R, int WARPS, int MINB, int VPL, bool FF = true>
+template <class R, int WARPS, int MINB, int VPL, bool FF = true, int PFV = 0>
 __global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_vec(RaggedParams p) {
   using B = typename R::B;
   using A = typename R::A;
@@ -940,8 +963,23 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_vec(RaggedParams p)
   int64_t open_rid = hrow;
   A open_val = R::id();
   __syncwarp();
+  // PFV > 0: lane 0 asks L2 to fetch the chunk PFV chunks ahead (one bulk prefetch, no registers or shared
+  // memory held), so the chunk's own loads hit L2 and more HBM bytes are in flight per warp
+  // PFV < 0: the same at distance -PFV, only while the previous chunk had no row start (inside long rows;
+  // short-row regions are issue-bound and skip the extra instructions)
+  constexpr int PFD = PFV < 0 ? -PFV : PFV;
+  bool pf_on = PFV > 0;
+  auto prefetch = [&](int64_t pb) {
+    if (PFV != 0 && lane == 0 && pf_on && pb < hi) {
+      const uint32_t bytes = (uint32_t)((hi - pb < CH ? hi - pb : CH) * sizeof(B)) & ~15u;
+      if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a + pb), "r"(bytes) : "memory");
+    }
+  };
   if (lo < hi) {
+#pragma unroll 1
+    for (int d = 1; d < PFV; ++d) prefetch(q0 + (int64_t)d * CH);
     for (int64_t Bc = q0; Bc < hi; Bc += CH) {
+      prefetch(Bc + (int64_t)PFD * CH);
       // valid positions of this chunk, relative to Bc: [rlo_c, rhi_c)
       const int rlo_c = (int)(lo > Bc ? lo - Bc : 0);
       const int rhi_c = (int)(hi - Bc < CH ? hi - Bc : CH);
@@ -1003,10 +1041,12 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_vec(RaggedParams p)
             }
           }
           open_val = R::op(open_val, R::warp(v));  // the open row's lane values join now
+          if (PFV < 0) pf_on = true;
           __syncwarp();
           continue;
         }
       }
+      if (PFV < 0) pf_on = false;
       // lane-local segmented fold, one pass: at every flagged element the running value (the segment that
       // ends there) is parked in the lane's own shared-memory column and the accumulator restarts
       A acc = R::id();

@@ -47,17 +47,17 @@ void run_flat(const char* name, void* buf, size_t bytes, void* ws, int sms, int 
   }
 }
 
-template <class R, int WARPS, int U, int HINT>
+template <class R, int WARPS, int U, int HINT, int PF = 0>
 void run_seg(const char* name, void* buf, void* out, int sms) {
   int maxb = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&maxb, k_seg_warp<R, WARPS, U, HINT>, WARPS * 32, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&maxb, k_seg_warp<R, WARPS, U, HINT, PF>, WARPS * 32, 0));
   const int64_t rows = 65536, cols = 4096;
   for (int cps = 1; cps <= maxb; cps *= 2) {
     SegParams p{buf, rows, cols, cols, 0, 0, out};
     const int grid = std::min<int64_t>(sms * cps, (rows + WARPS - 1) / WARPS);
-    float ms = time_ms([&] { k_seg_warp<R, WARPS, U, HINT><<<grid, WARPS * 32>>>(p); }, 10);
+    float ms = time_ms([&] { k_seg_warp<R, WARPS, U, HINT, PF><<<grid, WARPS * 32>>>(p); }, 10);
     CK(cudaGetLastError());
-    printf("seg  %-10s W=%2d U=%d H=%d cps=%d grid=%5d  %7.3f ms  %7.1f GB/s\n", name, WARPS, U, HINT, cps, grid, ms,
+    printf("seg  %-10s W=%2d U=%d H=%d PF=%d cps=%d grid=%5d  %7.3f ms  %7.1f GB/s\n", name, WARPS, U, HINT, PF, cps, grid, ms,
            (rows * cols * 4.0 + rows * 4) / ms / 1e6);
   }
 }
@@ -168,7 +168,7 @@ void run_flat_tma(const char* name, void* buf, size_t bytes, void* ws, int sms) 
 }
 
 
-template <class R, int U>
+template <class R, int U, int PF = 0>
 void run_2d(const char* name, void* buf, void* ws, int sms, int64_t rows, int64_t cols, int64_t stride, int cps) {
   using B = typename R::B;
   Params2D q{};
@@ -176,13 +176,13 @@ void run_2d(const char* name, void* buf, void* ws, int sms, int64_t rows, int64_
   q.f.tickets = (unsigned*)ws; q.f.world = 1;
   q.rows = rows; q.cols = cols; q.row_stride = stride;
   const int grid = sms * cps;
-  float ms = time_ms([&] { k_2d<R, 256, U><<<grid, 256>>>(q); }, 20);
+  float ms = time_ms([&] { k_2d<R, 256, U, PF><<<grid, 256>>>(q); }, 20);
   CK(cudaGetLastError());
   B res;
   CK(cudaMemcpy(&res, q.f.out, sizeof(B), cudaMemcpyDeviceToHost));
   const double bytes = (double)rows * cols * sizeof(B);
-  printf("2d %-6s %lldx%lld stride %lld U=%d cps=%d  %7.3f ms  %7.1f GB/s  result=%.17g\n", name,
-         (long long)rows, (long long)cols, (long long)stride, U, cps, ms, bytes / ms / 1e6, (double)res);
+  printf("2d %-6s %lldx%lld stride %lld U=%d PF=%d cps=%d  %7.3f ms  %7.1f GB/s  result=%.17g\n", name,
+         (long long)rows, (long long)cols, (long long)stride, U, PF, cps, ms, bytes / ms / 1e6, (double)res);
 }
 
 int main(int argc, char** argv) {
@@ -221,6 +221,28 @@ int main(int argc, char** argv) {
       run_flat<Red<IPM_ADD, IPM_F64>, 256, 8, 0>("f64+", buf, bytes, ws, sms);
       run_flat<Red<IPM_MAX, IPM_F64>, 256, 4, 0>("f64max", buf, bytes, ws, sms);
     }
+  }
+  if (mode == "pf") {  // L2 bulk prefetch of the warp's next row / item (PF=1) against none
+    for (int rep = 0; rep < 2; ++rep) {
+      printf("== segmented 65536 x 4096 f32 / f64 (32768 x 4096)\n");
+      run_seg<Red<IPM_ADD, IPM_F32>, 8, 8, 0, 0>("f32+", buf, out, sms);
+      run_seg<Red<IPM_ADD, IPM_F32>, 8, 8, 0, 1>("f32+", buf, out, sms);
+      run_seg<Red<IPM_ADD, IPM_F32>, 8, 4, 0, 1>("f32+", buf, out, sms);
+      run_seg<Red<IPM_BXOR, IPM_I32>, 8, 8, 0, 0>("i32^", buf, out, sms);
+      run_seg<Red<IPM_BXOR, IPM_I32>, 8, 8, 0, 1>("i32^", buf, out, sms);
+      printf("== 2-D\n");
+      for (int shape = 0; shape < 2; ++shape) {
+        const int64_t rows = shape == 0 ? 16384 : 262144, cols = shape == 0 ? 16000 : 1000,
+                      stride = shape == 0 ? 16384 : 1024;
+        run_2d<Red<IPM_ADD, IPM_F32>, 4, 0>("f32+", buf, ws, sms, rows, cols, stride, 4);
+        run_2d<Red<IPM_ADD, IPM_F32>, 4, 1>("f32+", buf, ws, sms, rows, cols, stride, 4);
+        run_2d<Red<IPM_ADD, IPM_F64>, 4, 0>("f64+", buf, ws, sms, rows / 2, cols, stride, 4);
+        run_2d<Red<IPM_ADD, IPM_F64>, 4, 1>("f64+", buf, ws, sms, rows / 2, cols, stride, 4);
+        run_2d<Red<IPM_BXOR, IPM_I32>, 4, 0>("i32^", buf, ws, sms, rows, cols, stride, 4);
+        run_2d<Red<IPM_BXOR, IPM_I32>, 4, 1>("i32^", buf, ws, sms, rows, cols, stride, 4);
+      }
+    }
+    return 0;
   }
   if (mode == "2d") {
     for (int shape = 0; shape < 3; ++shape) {

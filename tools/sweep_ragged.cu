@@ -27,13 +27,13 @@ static float time_ms(std::function<void()> f, int reps) {
 
 struct Data { void* a; int64_t* off; int64_t rows, nnz; void* out; void* ws; void* ref; int sms; };
 
-template <class R, int WARPS, int MINB, int VPL, bool FF = true>
+template <class R, int WARPS, int MINB, int VPL, bool FF = true, int PFV = 0>
 void run(const char* name, const Data& d) {
   using B = typename R::B;
-  CK(cudaFuncSetAttribute(k_ragged_vec<R, WARPS, MINB, VPL, FF>, cudaFuncAttributePreferredSharedMemoryCarveout,
+  CK(cudaFuncSetAttribute(k_ragged_vec<R, WARPS, MINB, VPL, FF, PFV>, cudaFuncAttributePreferredSharedMemoryCarveout,
                           (int)cudaSharedmemCarveoutMaxShared));
   int maxb = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&maxb, k_ragged_vec<R, WARPS, MINB, VPL, FF>, WARPS * 32, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&maxb, k_ragged_vec<R, WARPS, MINB, VPL, FF, PFV>, WARPS * 32, 0));
   const int blocks = d.sms * MINB;
   const int64_t nw = (int64_t)blocks * WARPS;
   RaggedParams p{};
@@ -42,7 +42,7 @@ void run(const char* name, const Data& d) {
   p.head_row = base; p.head_part = (uint64_t*)(base + 8192); p.tail_row = base + 2 * 8192;
   p.tail_part = (uint64_t*)(base + 3 * 8192);
   auto f = [&] {
-    k_ragged_vec<R, WARPS, MINB, VPL, FF><<<blocks, WARPS * 32>>>(p);
+    k_ragged_vec<R, WARPS, MINB, VPL, FF, PFV><<<blocks, WARPS * 32>>>(p);
     k_ragged_fix<R><<<(unsigned)((nw + 7) / 8), 256>>>(p, nw);
   };
   float ms = time_ms(f, 20);
@@ -58,7 +58,7 @@ void run(const char* name, const Data& d) {
     if (!(g == r || (g - r) * (g - r) <= 1e-20 * r * r + 1e-30)) ++bad;
   }
   const double bytes = d.nnz * sizeof(B) + (d.rows + 1) * 8.0 + d.rows * sizeof(B);
-  printf("%-4s W=%d MINB=%d VPL=%d FF=%d occ=%d  %7.3f ms  %7.1f GB/s  mismatches=%lld\n", name, WARPS, MINB, VPL, (int)FF, maxb, ms,
+  printf("%-4s W=%d MINB=%d VPL=%d FF=%d PFV=%d occ=%d  %7.3f ms  %7.1f GB/s  mismatches=%lld\n", name, WARPS, MINB, VPL, (int)FF, PFV, maxb, ms,
          bytes / ms / 1e6, (long long)bad);
 }
 
@@ -73,7 +73,11 @@ void all(const char* name, Data d) {
     run<R, 4, 8, 2, false>(name, Data{d.a, d.off, d.rows, d.nnz, d.ref, d.ws, d.ref, d.sms});
   }
   run<R, 4, 8, 2, true>(name, d);
-  run<R, 4, 8, 2, false>(name, d);
+  run<R, 4, 8, 2, true, 1>(name, d);
+  run<R, 4, 8, 2, true, 2>(name, d);
+  run<R, 4, 8, 2, true, -1>(name, d);
+  run<R, 4, 8, 2, true, -2>(name, d);
+  run<R, 4, 8, 2, true, -3>(name, d);
   run<R, 4, 8, 2, true>(name, d);
   CK(cudaFree(d.a)); CK(cudaFree(d.out)); CK(cudaFree(d.ref));
 }
