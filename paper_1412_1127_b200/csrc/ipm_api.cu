@@ -68,6 +68,28 @@ static int flat_ctas_per_sm() {
 }
 constexpr int SEG_WARPS = 8;
 constexpr int SEG_U = 8;
+// CTAs for k_seg_warp: warps take rows in grid-stride rounds, so when the rows do not fill the last round
+// some warps run one row longer while the rest idle (C3, 65536 rows: 592 CTAs -> 13.84 rows per warp, 6.75 TB/s;
+// 512 CTAs -> 16 rows per warp exactly, 6.92 TB/s, profiles/r01_sweep_segtail.txt). Take the CTA count in
+// [3/4, 1] x one resident wave (occ CTAs per SM) whose warps divide the rows most evenly (the smallest such
+// count), one row per warp if the rows fit in one wave.
+static int seg_grid(int64_t rows, int sms, int occ) {
+  const int64_t need = (rows + SEG_WARPS - 1) / SEG_WARPS;
+  const int64_t gmax = (int64_t)sms * occ;
+  if (need <= gmax) return (int)std::max<int64_t>(1, need);
+  const int64_t glo = std::max<int64_t>(1, gmax * 3 / 4);
+  int64_t best = gmax;
+  double best_eff = 0.0;
+  for (int64_t g = glo; g <= gmax; ++g) {
+    const int64_t nw = g * SEG_WARPS;
+    const double eff = (double)rows / (double)(((rows + nw - 1) / nw) * nw);
+    if (eff > best_eff + 1e-9) {
+      best_eff = eff;
+      best = g;
+    }
+  }
+  return (int)best;
+}
 constexpr int TMA_WARPS = 8, TMA_S = 4, TMA_CH = 4096;
 
 size_t esize(ipm_dtype dt) {
@@ -177,8 +199,13 @@ struct Launch {
       k_flat<R, FLAT_BLOCK, FLAT_U, 0, 0><<<grid, FLAT_BLOCK, 0, st>>>(p);
     }
   }
-  static void seg_warp(const SegParams& p, int grid, cudaStream_t st) {
-    k_seg_warp<R, SEG_WARPS, SEG_U><<<grid, SEG_WARPS * 32, 0, st>>>(p);
+  static void seg_warp(const SegParams& p, int sms, cudaStream_t st) {
+    static const int occ = [] {
+      int m = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m, k_seg_warp<R, SEG_WARPS, SEG_U>, SEG_WARPS * 32, 0);
+      return m > 0 ? m : 1;
+    }();
+    k_seg_warp<R, SEG_WARPS, SEG_U><<<seg_grid(p.rows, sms, occ), SEG_WARPS * 32, 0, st>>>(p);
   }
   static void ragged(const RaggedParams& p, int blocks, int64_t nw, cudaStream_t st) {
     // 25 KiB of static shared memory per CTA: ask for the largest carveout so 8 CTAs fit on an SM
@@ -224,7 +251,7 @@ struct Table {
   void (*flat)(const FlatParams&, dim3, cudaStream_t);
   void (*two_d)(const Params2D&, int, cudaStream_t);
   void (*ragged)(const RaggedParams&, int, int64_t, cudaStream_t);
-  void (*seg_warp)(const SegParams&, int, cudaStream_t);
+  void (*seg_warp)(const SegParams&, int, cudaStream_t);  // (params, SM count, stream)
   cudaError_t (*seg_tma)(const SegParams&, int, cudaStream_t);
   void (*seg_group)(const SegParams&, int, int, cudaStream_t);
   void (*finalize)(const uint64_t*, int, uint64_t, int, void*, cudaStream_t);
@@ -681,8 +708,7 @@ ipm_status ipm_reduce_segmented(ipm_op op, ipm_dtype dt, const void* dev, int64_
     const int64_t blocks = std::min<int64_t>((rows + TMA_WARPS - 1) / TMA_WARPS, (int64_t)sms);
     CK(t->seg_tma(p, (int)std::max<int64_t>(1, blocks), st));
   } else if (cols >= 32) {  // one warp per row, direct 256-bit loads
-    const int64_t blocks = std::min<int64_t>((rows + SEG_WARPS - 1) / SEG_WARPS, (int64_t)sms * 4);
-    t->seg_warp(p, (int)std::max<int64_t>(1, blocks), st);
+    t->seg_warp(p, sms, st);
   } else {           // G lanes per row, G = the power of two >= cols (capped at 16)
     int G = 1;
     while (G < cols && G < 16) G <<= 1;

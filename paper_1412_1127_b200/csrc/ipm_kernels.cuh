@@ -284,6 +284,7 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_flat(FlatParams p) {
       for (int k = 0; k < VW; ++k) acc[k] = R::op(acc[k], R::lift(v[u].w[k]));
   };
   if (SCHED == 0) {
+    #pragma unroll 1
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) tile(t);
   } else if (SCHED == 3) {  // static grid-stride, software-pipelined: the next tile's loads are issued first
     int64_t t = blockIdx.x;
@@ -292,6 +293,7 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_flat(FlatParams p) {
 #pragma unroll
       for (int u = 0; u < U; ++u) nx[u] = ldv<HINT>(vp + t * TILE + threadIdx.x + u * BLOCK);
     }
+    #pragma unroll 1
     for (; t < ntiles; t += gridDim.x) {
       VT cu[U];
 #pragma unroll
@@ -308,6 +310,7 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_flat(FlatParams p) {
     }
   } else if (SCHED == 1) {
     const int64_t t1 = (ntiles * (blockIdx.x + 1)) / gridDim.x;
+    #pragma unroll 1
     for (int64_t t = (ntiles * blockIdx.x) / gridDim.x; t < t1; ++t) tile(t);
   } else {
     __shared__ long long s_next;
@@ -424,6 +427,7 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_flat_guided(FlatParams 
     VT nx[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) nx[u] = ldv(vp + first * TILE + threadIdx.x + u * BLOCK);
+#pragma unroll 1
     for (int64_t k = 0; k < count; ++k) {
       VT cu[U];
 #pragma unroll
@@ -542,7 +546,7 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_2d(Params2D q) {
   A acc[VW];
 #pragma unroll
   for (int k = 0; k < VW; ++k) acc[k] = R::id();
-  for (int64_t it = gw; it < items; it += nw) {
+    for (int64_t it = gw; it < items; it += nw) {
     if (PF && lane == 0 && it + nw < items) {  // the warp's next item (row, chunk) into L2
       int64_t rn = r + dr, cn = c + dc;
       if (cn >= per_row) {
@@ -612,6 +616,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_seg_warp(SegParams p) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5);
   const int64_t nw = (int64_t)gridDim.x * WARPS;
+  #pragma unroll 1
   for (int64_t r = gw; r < p.rows; r += nw) {
     if (PF && lane == 0 && r + nw < p.rows)  // the warp's next row into L2
       l2_prefetch((const B*)p.a + (r + nw) * p.row_stride, p.cols * (int64_t)sizeof(B));
@@ -626,6 +631,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_seg_warp(SegParams p) {
 #pragma unroll
     for (int k = 0; k < VW; ++k) acc[k] = R::id();
     int64_t i = lane;
+    #pragma unroll 1
     for (; i + (U - 1) * 32 < nv; i += U * 32) {
       VT v[U];
 #pragma unroll

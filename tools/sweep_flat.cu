@@ -222,6 +222,52 @@ int main(int argc, char** argv) {
       run_flat<Red<IPM_MAX, IPM_F64>, 256, 4, 0>("f64max", buf, bytes, ws, sms);
     }
   }
+  if (mode == "segdt") {  // old product grid (sms * 4) vs the balanced choice (ipm_api.cu seg_grid), per fold
+    auto go = [&](auto red, const char* name, int64_t rows) {
+      using R = decltype(red);
+      using B = typename R::B;
+      int occ = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_seg_warp<R, 8, 8, 0>, 256, 0));
+      const int64_t cols = 4096;
+      const int64_t gmax = (int64_t)sms * occ, glo = gmax * 3 / 4;
+      int64_t best = gmax; double be = 0;
+      for (int64_t g = glo; g <= gmax; ++g) {
+        const int64_t nw = g * 8;
+        const double e = (double)rows / (double)(((rows + nw - 1) / nw) * nw);
+        if (e > be + 1e-9) { be = e; best = g; }
+      }
+      for (int rep = 0; rep < 2; ++rep)
+        for (int64_t grid : {(int64_t)sms * 4, best}) {
+          SegParams p{buf, rows, cols, cols, 0, 0, out};
+          float ms = time_ms([&] { k_seg_warp<R, 8, 8, 0><<<(int)grid, 256>>>(p); }, 20);
+          CK(cudaGetLastError());
+          printf("segdt %-6s occ=%d rows=%lld grid=%5lld rows/warp=%.2f  %7.3f ms  %7.1f GB/s\n", name, occ,
+                 (long long)rows, (long long)grid, rows / (grid * 8.0), ms, (rows * cols * (double)sizeof(B) + rows * sizeof(B)) / ms / 1e6);
+        }
+    };
+    go(Red<IPM_ADD, IPM_F32>{}, "f32+", 65536);
+    go(Red<IPM_MAX, IPM_F32>{}, "f32max", 65536);
+    go(Red<IPM_ADD, IPM_F64>{}, "f64+", 65536);
+    go(Red<IPM_MUL, IPM_F64>{}, "f64*", 65536);
+    go(Red<IPM_BXOR, IPM_I32>{}, "i32^", 65536);
+    go(Red<IPM_MIN, IPM_I64>{}, "i64min", 65536);
+    go(Red<IPM_ADD, IPM_F32>{}, "f32+", 50000);
+    go(Red<IPM_ADD, IPM_F32>{}, "f32+", 100003);
+    return 0;
+  }
+  if (mode == "segtail") {  // C3: rows per warp exactly equal (grid 512 / 1024) vs the product's sms * 4
+    for (int rep = 0; rep < 3; ++rep) {
+      const int64_t rows = 65536, cols = 4096;
+      for (int grid : {592, 512, 1024, 1184, 256 * 3}) {
+        SegParams p{buf, rows, cols, cols, 0, 0, out};
+        float ms = time_ms([&] { k_seg_warp<Red<IPM_ADD, IPM_F32>, 8, 8, 0><<<grid, 256>>>(p); }, 20);
+        CK(cudaGetLastError());
+        printf("segtail f32+ W=8 U=8 grid=%5d rows/warp=%.2f  %7.3f ms  %7.1f GB/s\n", grid, rows / (grid * 8.0), ms,
+               (rows * cols * 4.0 + rows * 4) / ms / 1e6);
+      }
+    }
+    return 0;
+  }
   if (mode == "pf") {  // L2 bulk prefetch of the warp's next row / item (PF=1) against none
     for (int rep = 0; rep < 2; ++rep) {
       printf("== segmented 65536 x 4096 f32 / f64 (32768 x 4096)\n");
