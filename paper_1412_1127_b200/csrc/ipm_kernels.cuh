@@ -597,93 +597,6 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_2d(Params2D q) {
   grid_finish<R, BLOCK>(q.f, 0, cta, sm);
 }
 
-// Software-pipelined variant: the next item's loads are issued before the current item is folded (as in
-// k_flat_guided), so a warp keeps 32*U vectors in flight across item boundaries. The widened float32 + * fold
-// keeps NA = 2 float64 accumulators instead of VW = 8 (element k of a vector into acc[k % NA]): the registers of a
-// second in-flight item fit under the 64-register cap without spilling.
-template <class R, int BLOCK, int U, int MINB = 1024 / BLOCK>
-__global__ void __launch_bounds__(BLOCK, MINB) k_2d_pipe(Params2D q) {
-  using B = typename R::B;
-  using A = typename R::A;
-  using VT = typename Vec<B>::T;
-  constexpr int VW = Vec<B>::W;
-  constexpr int NA = sizeof(A) > sizeof(B) ? 2 : VW;
-  constexpr int64_t CHV = 32 * U;
-  __shared__ A sm[BLOCK / 32];
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = (int64_t)blockIdx.x * (BLOCK / 32) + (threadIdx.x >> 5);
-  const int64_t nw = (int64_t)gridDim.x * (BLOCK / 32);
-  const int64_t maxv = q.cols / VW;
-  const int64_t per_row = maxv > 0 ? (maxv + CHV - 1) / CHV : 1;
-  const int64_t items = q.rows * per_row;
-  const int64_t dr = nw / per_row, dc = nw - dr * per_row;
-  int64_t r = gw / per_row, c = gw - r * per_row;
-  A acc[NA];
-#pragma unroll
-  for (int k = 0; k < NA; ++k) acc[k] = R::id();
-  const B* base = (const B*)q.f.a;
-  auto head_of = [&](const B* a) {
-    int64_t h = (int64_t)(((32u - ((uintptr_t)a & 31u)) & 31u) / sizeof(B));
-    return h > q.cols ? q.cols : h;
-  };
-  VT nx[U];
-  // issue the loads of item (r_, c_) if it is a full item; returns whether it was
-  auto issue = [&](int64_t r_, int64_t c_) -> bool {
-    const B* a = base + r_ * q.row_stride;
-    const int64_t h = head_of(a);
-    const int64_t nv = (q.cols - h) / VW;
-    if (c_ * CHV + CHV > nv) return false;
-    const VT* vp = (const VT*)(a + h) + c_ * CHV + lane;
-#pragma unroll
-    for (int u = 0; u < U; ++u) nx[u] = ldv(vp + u * 32);
-    return true;
-  };
-  bool nfull = gw < items ? issue(r, c) : false;
-#pragma unroll 1
-  for (int64_t it = gw; it < items; it += nw) {
-    VT cu[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) cu[u] = nx[u];
-    const bool full = nfull;
-    const int64_t rc = r, cc = c;
-    r += dr;
-    c += dc;
-    if (c >= per_row) {
-      c -= per_row;
-      ++r;
-    }
-    if (it + nw < items) nfull = issue(r, c);
-    if (full) {
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-#pragma unroll
-        for (int k = 0; k < VW; ++k) acc[k % NA] = R::op(acc[k % NA], R::lift(cu[u].w[k]));
-    }
-    const B* a = base + rc * q.row_stride;
-    const int64_t h = head_of(a);
-    const int64_t nv = (q.cols - h) / VW;
-    if (!full) {  // the row's last, partial item
-      const VT* vp = (const VT*)(a + h);
-      for (int64_t i = cc * CHV + lane; i < nv; i += 32) {
-        const VT v = ldv(vp + i);
-#pragma unroll
-        for (int k = 0; k < VW; ++k) acc[k % NA] = R::op(acc[k % NA], R::lift(v.w[k]));
-      }
-    }
-    if (cc == 0) {
-      const int64_t tail0 = h + nv * VW;
-      if (lane < h) acc[0] = R::op(acc[0], R::lift(lds(a + lane)));
-      if (lane < q.cols - tail0) acc[NA - 1] = R::op(acc[NA - 1], R::lift(lds(a + tail0 + lane)));
-    }
-  }
-#pragma unroll
-  for (int s2 = NA / 2; s2 > 0; s2 >>= 1)
-#pragma unroll
-    for (int k = 0; k < s2; ++k) acc[k] = R::op(acc[k], acc[k + s2]);
-  A cta = block_reduce<R, BLOCK>(acc[0], sm);
-  grid_finish<R, BLOCK>(q.f, 0, cta, sm);
-}
-
 // ------------------------------------------------------------------------------------------ segmented
 struct SegParams {
   const void* a;

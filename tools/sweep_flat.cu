@@ -168,23 +168,6 @@ void run_flat_tma(const char* name, void* buf, size_t bytes, void* ws, int sms) 
 }
 
 
-template <class R, int U, int MINB = 4>
-void run_2dp(const char* name, void* buf, void* ws, int sms, int64_t rows, int64_t cols, int64_t stride, int cps) {
-  using B = typename R::B;
-  Params2D q{};
-  q.f.a = buf; q.f.mode = MODE_RESULT; q.f.out = (char*)ws + 4096; q.f.partials = (uint64_t*)((char*)ws + 8192);
-  q.f.tickets = (unsigned*)ws; q.f.world = 1;
-  q.rows = rows; q.cols = cols; q.row_stride = stride;
-  const int grid = sms * cps;
-  float ms = time_ms([&] { k_2d_pipe<R, 256, U, MINB><<<grid, 256>>>(q); }, 20);
-  CK(cudaGetLastError());
-  B res;
-  CK(cudaMemcpy(&res, q.f.out, sizeof(B), cudaMemcpyDeviceToHost));
-  const double bytes = (double)rows * cols * sizeof(B);
-  printf("2dpipe %-6s %lldx%lld stride %lld U=%d MINB=%d cps=%d  %7.3f ms  %7.1f GB/s  result=%.17g\n", name,
-         (long long)rows, (long long)cols, (long long)stride, U, MINB, cps, ms, bytes / ms / 1e6, (double)res);
-}
-
 template <class R, int U, int PF = 0>
 void run_2d(const char* name, void* buf, void* ws, int sms, int64_t rows, int64_t cols, int64_t stride, int cps) {
   using B = typename R::B;
@@ -238,27 +221,6 @@ int main(int argc, char** argv) {
       run_flat<Red<IPM_ADD, IPM_F64>, 256, 8, 0>("f64+", buf, bytes, ws, sms);
       run_flat<Red<IPM_MAX, IPM_F64>, 256, 4, 0>("f64max", buf, bytes, ws, sms);
     }
-  }
-  if (mode == "2dpipe") {  // k_2d (product) vs the software-pipelined k_2d_pipe (MINB CTAs of 256 per SM)
-    for (int rep = 0; rep < 2; ++rep)
-      for (int shape = 0; shape < 3; ++shape) {
-        const int64_t rows = shape == 0 ? 16384 : shape == 1 ? 262144 : 4096, cols = shape == 0 ? 16000 : shape == 1 ? 1000 : 65000,
-                      stride = shape == 0 ? 16384 : shape == 1 ? 1024 : 65536;
-        run_2d<Red<IPM_ADD, IPM_F32>, 4>("f32+", buf, ws, sms, rows, cols, stride, 4);
-        run_2dp<Red<IPM_ADD, IPM_F32>, 2, 3>("f32+", buf, ws, sms, rows, cols, stride, 3);
-        run_2dp<Red<IPM_ADD, IPM_F32>, 4, 2>("f32+", buf, ws, sms, rows, cols, stride, 2);
-        run_2dp<Red<IPM_ADD, IPM_F32>, 4, 3>("f32+", buf, ws, sms, rows, cols, stride, 3);
-        run_2d<Red<IPM_MAX, IPM_F32>, 4>("f32max", buf, ws, sms, rows, cols, stride, 4);
-        run_2dp<Red<IPM_MAX, IPM_F32>, 2, 3>("f32max", buf, ws, sms, rows, cols, stride, 3);
-        run_2dp<Red<IPM_MAX, IPM_F32>, 4, 2>("f32max", buf, ws, sms, rows, cols, stride, 2);
-        run_2d<Red<IPM_ADD, IPM_F64>, 4>("f64+", buf, ws, sms, rows / 2, cols, stride, 4);
-        run_2dp<Red<IPM_ADD, IPM_F64>, 2, 3>("f64+", buf, ws, sms, rows / 2, cols, stride, 3);
-        run_2dp<Red<IPM_ADD, IPM_F64>, 4, 2>("f64+", buf, ws, sms, rows / 2, cols, stride, 2);
-        run_2d<Red<IPM_BXOR, IPM_I32>, 4>("i32^", buf, ws, sms, rows, cols, stride, 4);
-        run_2dp<Red<IPM_BXOR, IPM_I32>, 2, 3>("i32^", buf, ws, sms, rows, cols, stride, 3);
-        run_2dp<Red<IPM_BXOR, IPM_I32>, 4, 2>("i32^", buf, ws, sms, rows, cols, stride, 2);
-      }
-    return 0;
   }
   if (mode == "segdt") {  // old product grid (sms * 4) vs the balanced choice (ipm_api.cu seg_grid), per fold
     auto go = [&](auto red, const char* name, int64_t rows) {
