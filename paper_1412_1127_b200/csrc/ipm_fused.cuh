@@ -108,7 +108,7 @@ __device__ __forceinline__ void fused_finish(const FusedParams& p, int v, typena
 
 // TWO: read y as a second stream. VEC: both streams share the same alignment mod 32 (256-bit loads); else
 // element loads (coalesced across the warp).
-template <class S, class C0, class C1, class C2, class C3, bool TWO, bool VEC, int BLOCK, int U>
+template <class S, class C0, class C1, class C2, class C3, bool TWO, bool VEC, int BLOCK, int U, bool PIPE = false>
 __global__ void __launch_bounds__(BLOCK) k_fused(FusedParams p) {
   using B = typename S::B;
   using Acc = typename S::Acc;
@@ -131,7 +131,36 @@ __global__ void __launch_bounds__(BLOCK) k_fused(FusedParams p) {
     const VT* xv = (const VT*)(x + head);
     const VT* yv = (const VT*)(y + head);
     const int64_t ntiles = nv / TILE;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    // PIPE: the next tile's loads are issued before this one is folded (measured equal or slower than the plain
+    // loop: the extra registers cost resident CTAs, profiles/r01_sweep_fused_pipe.txt; the product uses PIPE=false)
+    if (PIPE && (int64_t)blockIdx.x < ntiles) {
+      VT na[U], nb[TWO ? U : 1];
+      auto issue = [&](int64_t t) {
+        const int64_t base = t * TILE + threadIdx.x;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          na[u] = ldv(xv + base + u * BLOCK);
+          if (TWO) nb[TWO ? u : 0] = ldv(yv + base + u * BLOCK);
+        }
+      };
+      issue(blockIdx.x);
+#pragma unroll 1
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        VT a[U], b[TWO ? U : 1];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          a[u] = na[u];
+          if (TWO) b[TWO ? u : 0] = nb[TWO ? u : 0];
+        }
+        if (t + gridDim.x < ntiles) issue(t + gridDim.x);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int k = 0; k < VW; ++k)
+            acc[k & 1] = S::op(acc[k & 1], S::val(a[u].w[k], TWO ? b[TWO ? u : 0].w[k] : a[u].w[k]));
+      }
+    }
+    for (int64_t t = blockIdx.x; !PIPE && t < ntiles; t += gridDim.x) {
       const int64_t base = t * TILE + threadIdx.x;
       VT a[U], b[TWO ? U : 1];
 #pragma unroll
