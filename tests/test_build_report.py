@@ -1,0 +1,42 @@
+"""The product's hot kernels compile without register spills (ptxas -v report written by tools/build.py).
+
+A spill inside a streaming loop turns into local-memory traffic per tile: int64 max/min/&& ran 10-25 % slower
+until the pipelined tile loop of k_flat_guided stopped spilling (profiles/r01_probe_int64_after.txt)."""
+import os
+import re
+import subprocess
+
+import pytest
+
+from tools import build
+
+HOT = ("k_flat_guided", "k_ragged_vec", "k_ragged_fix", "k_fused", "dist_exchange", "k_finalize")
+
+
+def _report():
+    lib = os.path.join(build.ROOT, "paper_1412_1127_b200", "libipm.so")
+    if not os.path.exists(build.PTXAS_LOG) or not os.path.exists(lib):
+        pytest.skip("no ptxas report: run tools/build.py (build_ipm) first")
+    if os.path.getmtime(build.PTXAS_LOG) + 1 < os.path.getmtime(lib):
+        pytest.skip("ptxas report older than libipm.so")
+    out, cur = {}, None
+    for line in open(build.PTXAS_LOG):
+        m = re.search(r"Function properties for (\S+)", line)
+        if m:
+            cur = m.group(1)
+        m = re.search(r"(\d+) bytes spill stores, (\d+) bytes spill loads", line)
+        if m and cur:
+            out[cur] = (int(m.group(1)), int(m.group(2)))
+            cur = None
+    return out
+
+
+def test_hot_kernels_do_not_spill():
+    rep = _report()
+    keys = list(rep)
+    dem = subprocess.run(["c++filt"], input="\n".join(keys), capture_output=True, text=True).stdout.split("\n")
+    names = {k: (dem[i] if i < len(dem) and dem[i] else k) for i, k in enumerate(keys)}
+    hot = {k: v for k, v in rep.items() if any(h in names[k] for h in HOT)}
+    assert len([k for k in hot if "k_flat_guided" in names[k]]) == 30  # one per legal (op, dtype) pair
+    bad = {names[k]: v for k, v in hot.items() if v != (0, 0)}
+    assert not bad, bad

@@ -72,12 +72,19 @@ def build_ipm(force: bool = False, extra: list[str] | None = None) -> str:
     if force or extra or _stale(out, srcs):
         nccl = _nccl_dir()
         cus = [s for s in srcs if s.endswith(".cu")]
-        _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xptxas", "-v", "-Xcompiler", "-fPIC,-Wall",
+        r = _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xptxas", "-v", "-Xcompiler", "-fPIC,-Wall",
               "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nccl, "include"),
               *(extra or []), "-shared", "-o", out, *cus,
               "-L", os.path.join(nccl, "lib"), "-l:libnccl.so.2", f"-Xlinker=-rpath={os.path.join(nccl, 'lib')}",
               "-lcudart"])
+        # ptxas resource report (registers, spills per kernel): tests/test_build_report.py checks the hot kernels
+        os.makedirs(os.path.join(ROOT, "build"), exist_ok=True)
+        with open(PTXAS_LOG, "w") as f:
+            f.write(r.stdout + r.stderr)
     return out
+
+
+PTXAS_LOG = os.path.join(ROOT, "build", "ptxas_libipm.txt")
 
 
 def build_tools(force: bool = False) -> None:
