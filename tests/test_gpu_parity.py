@@ -216,7 +216,9 @@ def test_cuda_graph_capture(ipm):
 
 SEG_SHAPES = [(0, 5), (1, 0), (7, 0), (1, 1), (7, 3), (1000, 1), (1000, 3), (1000, 31), (1000, 32), (1000, 33),
               (257, 4095), (257, 4096), (65, 4097), (3, 1 << 20), (1, (1 << 21) + 5), (40, 70_001),
-              (700, 1025), (1200, 4099), (65536, 3), (65536, 33), (65536, 0)]
+              (700, 1025), (1200, 4099), (65536, 3), (65536, 33), (65536, 0),
+              # more rows than one resident wave of warps: the CTA count is chosen to divide the rows evenly
+              (9473, 40), (50000, 36)]
 
 
 @pytest.fixture(params=["auto", "warp", "tma"])
