@@ -108,8 +108,12 @@ __device__ __forceinline__ void fused_finish(const FusedParams& p, int v, typena
 
 // TWO: read y as a second stream. VEC: both streams share the same alignment mod 32 (256-bit loads); else
 // element loads (coalesced across the warp).
-template <class S, class C0, class C1, class C2, class C3, bool TWO, bool VEC, int BLOCK, int U, bool PIPE = false>
-__global__ void __launch_bounds__(BLOCK) k_fused(FusedParams p) {
+// MINB: the launch-bounds minimum of resident CTAs per SM. 0 (the product) states none: ptxas then gives the
+// float32 x*y kernel 48 registers (4 CTAs per SM resident, 7.03-7.12 TB/s); MINB = 4 made it 61 registers and
+// 4 % slower, MINB = 1 left 1 resident CTA (profiles/r01_sweep_fused_pipe.txt)
+template <class S, class C0, class C1, class C2, class C3, bool TWO, bool VEC, int BLOCK, int U, bool PIPE = false,
+          int MINB = 0>
+__global__ void __launch_bounds__(BLOCK, MINB) k_fused(FusedParams p) {
   using B = typename S::B;
   using Acc = typename S::Acc;
   using VT = typename Vec<B>::T;

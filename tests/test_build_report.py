@@ -40,3 +40,4 @@ def test_hot_kernels_do_not_spill():
     assert len([k for k in hot if "k_flat_guided" in names[k]]) == 30  # one per legal (op, dtype) pair
     bad = {names[k]: v for k, v in hot.items() if v != (0, 0)}
     assert not bad, bad
+

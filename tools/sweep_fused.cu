@@ -24,21 +24,21 @@ static float time_ms(std::function<void()> f, int reps) {
   return v[v.size() / 2];
 }
 
-template <class S, class C0, class C1, class C2, class C3, bool TWO, int U, bool PIPE>
+template <class S, class C0, class C1, class C2, class C3, bool TWO, int U, bool PIPE, int MINB = 4>
 void run(const char* name, void* x, void* y, int64_t n, void* ws, int sms, int cps) {
   using B = typename S::B;
   FusedParams p{};
   p.x = x; p.y = TWO ? y : nullptr; p.n = n; p.has_init = 0; p.out = (char*)ws + 4096;
   p.partials = (uint64_t*)((char*)ws + 8192); p.ticket = (unsigned*)ws;
   int occ = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused<S, C0, C1, C2, C3, TWO, true, 256, U, PIPE>, 256, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused<S, C0, C1, C2, C3, TWO, true, 256, U, PIPE, MINB>, 256, 0));
   const int grid = sms * cps;
-  float ms = time_ms([&] { k_fused<S, C0, C1, C2, C3, TWO, true, 256, U, PIPE><<<grid, 256>>>(p); }, 20);
+  float ms = time_ms([&] { k_fused<S, C0, C1, C2, C3, TWO, true, 256, U, PIPE, MINB><<<grid, 256>>>(p); }, 20);
   CK(cudaGetLastError());
   B out[4];
   CK(cudaMemcpy(out, p.out, sizeof out, cudaMemcpyDeviceToHost));
   const double bytes = (double)n * sizeof(B) * (TWO ? 2 : 1);
-  printf("fused %-8s U=%d PIPE=%d occ=%d cps=%d  %7.3f ms  %7.1f GB/s  out0=%.17g\n", name, U, (int)PIPE, occ, cps, ms,
+  printf("fused %-8s U=%d PIPE=%d MINB=%d occ=%d cps=%d  %7.3f ms  %7.1f GB/s  out0=%.17g\n", name, U, (int)PIPE, MINB, occ, cps, ms,
          bytes / ms / 1e6, (double)out[0]);
 }
 
@@ -60,17 +60,13 @@ int main() {
   using D_ADDX = Comp<Red<IPM_ADD, IPM_F64>, EX>;
   using D_ADDXX = Comp<Red<IPM_ADD, IPM_F64>, EXX>;
   using DSS = Sig<D_ADDX, D_ADDXX>;
-  for (int rep = 0; rep < 2; ++rep) {
-    run<STATS, ADDX, ADDXX, MINX, MAXX, false, 2, false>("stats", x, y, n, ws, sms, 4);
-    run<STATS, ADDX, ADDXX, MINX, MAXX, false, 2, true>("stats", x, y, n, ws, sms, 4);
-    run<STATS, ADDX, ADDXX, MINX, MAXX, false, 1, true>("stats", x, y, n, ws, sms, 4);
-    run<SS, ADDX, ADDXX, NoComp, NoComp, false, 2, false>("sumsq", x, y, n, ws, sms, 4);
-    run<SS, ADDX, ADDXX, NoComp, NoComp, false, 2, true>("sumsq", x, y, n, ws, sms, 4);
-    run<DOT, ADDXY, NoComp, NoComp, NoComp, true, 2, false>("dot", x, y, n, ws, sms, 4);
-    run<DOT, ADDXY, NoComp, NoComp, NoComp, true, 2, true>("dot", x, y, n, ws, sms, 4);
-    run<DOT, ADDXY, NoComp, NoComp, NoComp, true, 1, true>("dot", x, y, n, ws, sms, 4);
-    run<DSS, D_ADDX, D_ADDXX, NoComp, NoComp, false, 2, false>("f64sumsq", x, y, n, ws, sms, 4);
-    run<DSS, D_ADDX, D_ADDXX, NoComp, NoComp, false, 2, true>("f64sumsq", x, y, n, ws, sms, 4);
+  for (int rep = 0; rep < 3; ++rep) {
+    run<DOT, ADDXY, NoComp, NoComp, NoComp, true, 2, false, 0>("dot", x, y, n, ws, sms, 4);
+    run<DOT, ADDXY, NoComp, NoComp, NoComp, true, 2, false, 4>("dot", x, y, n, ws, sms, 4);
+    run<DOT, ADDXY, NoComp, NoComp, NoComp, true, 2, false, 5>("dot", x, y, n, ws, sms, 5);
+    run<STATS, ADDX, ADDXX, MINX, MAXX, false, 2, false, 0>("stats", x, y, n, ws, sms, 4);
+    run<STATS, ADDX, ADDXX, MINX, MAXX, false, 2, false, 4>("stats", x, y, n, ws, sms, 4);
+    run<STATS, ADDX, ADDXX, MINX, MAXX, false, 2, false, 5>("stats", x, y, n, ws, sms, 5);
   }
   return 0;
 }
