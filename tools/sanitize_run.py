@@ -22,7 +22,8 @@ for dt in TD:
                 ipm.reduce(op, x, init=np.array(1, dtype=x.cpu().numpy().dtype)[()])
     for kern in ("ldg", "tma"):
         ipm.set_option("seg_kernel", kern)
-        for rows, cols, stride in [(5, 3, 4), (33, 100, 103), (9, 4097, 4100), (2, 40_000, 40_001), (300, 64, 64)]:
+        for rows, cols, stride in [(5, 3, 4), (33, 100, 103), (9, 4097, 4100), (2, 40_000, 40_001), (300, 64, 64),
+                                  (6000, 40, 40)]:  # more rows than one resident wave of warps
             x = torch.empty((rows - 1) * stride + cols + 3, dtype=TD[dt], device="cuda")
             ipmgen.fill_device(ipmgen.Spec(dt, x.numel(), "random", seed=1), x.data_ptr(), 0, x.numel(),
                                torch.cuda.current_stream().cuda_stream)
