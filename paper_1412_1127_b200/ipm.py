@@ -14,7 +14,7 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libipm.so")
+LIB_PATH = os.environ.get("IPM_LIB", os.path.join(_HERE, "libipm.so"))  # IPM_LIB: A/B of two builds (tools/ab_lib.py)
 
 # operator names follow the clause syntax `reduction(op:var)` (OpenACC; SPEC.md:110 plus the BASELINE.json ops)
 OPS = {"+": 0, "*": 1, "max": 2, "min": 3, "&": 4, "|": 5, "^": 6, "&&": 7, "||": 8}
