@@ -8,7 +8,10 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CASES = [("flat", "float32", "+", 1 << 28), ("flat", "float64", "max", 1 << 28), ("flat", "int64", "&&", 1 << 30),
          ("seg", "float32", "+", 65536 * 4096), ("2d", "float32", "+", 16384 * 16384),
-         ("stats", "float32", "+", 1 << 28)]
+         ("stats", "float32", "+", 1 << 28), ("2d", "float32", "max", 16384 * 16384), ("2d", "int32", "^", 16384 * 16384),
+         ("2d", "float64", "+", 16384 * 16384)]
+if os.environ.get("AB_CASES"):  # e.g. AB_CASES=2d: only cases of that kind
+    CASES = [c for c in CASES if c[0] in os.environ["AB_CASES"].split(",")]
 
 
 def child():
@@ -18,7 +21,7 @@ def child():
     import torch
     import ipmgen
     from paper_1412_1127_b200 import ipm
-    TD = {"float32": torch.float32, "float64": torch.float64, "int64": torch.int64}
+    TD = {"float32": torch.float32, "float64": torch.float64, "int64": torch.int64, "int32": torch.int32}
     out = {}
     for kind, dt, op, n in CASES:
         x = torch.empty(n, dtype=TD[dt], device="cuda")
@@ -31,7 +34,7 @@ def child():
             elif kind == "seg":
                 ipm.reduce_segmented(op, x.view(65536, 4096))
             elif kind == "2d":
-                ipm.reduce_2d(op, x.view(16384, 16384)[:, :16000])
+                ipm.reduce_2d(op, x.view(-1, 16384)[:, :16000])
             else:
                 ipm.reduce_fused_async("stats", x)
         t0 = time.perf_counter()
