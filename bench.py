@@ -164,6 +164,31 @@ def cpu_baseline_oracle(x_dev, seconds_target=10.0):
                       f"{dt:.1f} s; host has {host_cores()} cores", "elements_per_s": m / dt}
 
 
+def cpu_native_omp(x_dev, reps=3):
+    """BASELINE.md's CPU native baseline: OpenMP `parallel for simd reduction(+:s)` in the input's native precision
+    (float32 accumulators) on all host cores (tools/cpu_omp.c), over the same bounded prefix as the oracle."""
+    import ctypes
+
+    lib_path = os.path.join(ROOT, "tools", "bin", "libcpu_omp.so")
+    if not os.path.exists(lib_path):
+        return {"value": None, "unit": "GB/s", "kind": "openmp", "error": "tools/bin/libcpu_omp.so not built"}
+    L = ctypes.CDLL(lib_path)
+    L.cpu_omp_sum_f32.restype = ctypes.c_float
+    L.cpu_omp_sum_f32.argtypes = [ctypes.c_void_p, ctypes.c_int64]
+    n = min(x_dev.numel(), 1 << 30)
+    a = x_dev[:n].cpu().numpy()
+    L.cpu_omp_sum_f32(a.ctypes.data, n)  # warm (first touch of the threads)
+    best, res = None, None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        res = L.cpu_omp_sum_f32(a.ctypes.data, n)
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    return {"value": n * ELEM / best / 1e9, "unit": "GB/s", "cores": int(L.cpu_omp_threads()), "kind": "openmp",
+            "sample": f"first {n} elements of rank 0's C5 shard (host copy), float32 accumulators, best of {reps}",
+            "result": float(res), "elements_per_s": n / best}
+
+
 def suite(ipm, torch, ipmgen, peak):
     """The other BASELINE configs, device-timed with the library's per-kernel events (rank 0, N=1)."""
     out = {}
@@ -459,10 +484,15 @@ def run_ours(args, rank, world, local_rank):
 
     if rank == 0:
         cpu = None  # the oracle baseline runs at N = 1 only (a bounded host sample; the same at any N)
+        cpu_omp = None
         if not args.no_cpu and world == 1:
             xs = torch.empty(min(n_shard, 1 << 30), dtype=torch.float32, device="cuda")
             ipmgen.fill_device(spec, xs.data_ptr(), lo, xs.numel(), torch.cuda.current_stream().cuda_stream)
             cpu = cpu_baseline_oracle(xs)
+            try:
+                cpu_omp = cpu_native_omp(xs)
+            except Exception as ex:  # a baseline only: never fail the bench line over it
+                cpu_omp = {"value": None, "unit": "GB/s", "kind": "openmp", "error": repr(ex)[:200]}
             del xs
         st = suite(ipm, torch, ipmgen, peak) if (world == 1 and not args.no_suite) else None
         traffic = None
@@ -492,7 +522,7 @@ def run_ours(args, rank, world, local_rank):
                          "vs_8TBs_spec": achieved / 8000.0},
             "step_stats_ms": {"harmonic_mean": harmonic(step_ms), "median": statistics.median(step_ms),
                               "min": min(step_ms)},
-            "cpu_baseline": cpu, "e2e": e2e,
+            "cpu_baseline": cpu, "cpu_native": cpu_omp, "e2e": e2e,
             "gpu_launches": (1 if comm_fused else 2) * args.steps,
             "gpu_launches_note": ("per step: 1 k_flat_guided (reduction + NVLink peer-memory exchange in one kernel)"
                                   if comm_fused else "per step: 1 k_flat_guided + 1 k_finalize (plus NCCL's own "

@@ -100,11 +100,24 @@ def build_tools(force: bool = False) -> None:
             sys.stderr.write(f"optional tool not built: {e}\n")
 
 
+def build_cpu_omp(force: bool = False) -> None:
+    """The OpenMP CPU baseline (BASELINE.md "CPU native baseline") that bench.py times at N = 1. Optional."""
+    out = os.path.join(ROOT, "tools", "bin", "libcpu_omp.so")
+    src = os.path.join(ROOT, "tools", "cpu_omp.c")
+    if force or _stale(out, [src]):
+        os.makedirs(os.path.dirname(out), exist_ok=True)
+        try:
+            _run(["gcc", "-std=c11", "-O3", "-march=x86-64-v2", "-fopenmp", "-fPIC", "-shared", "-o", out, src])
+        except RuntimeError as e:
+            sys.stderr.write(f"optional CPU baseline not built: {e}\n")
+
+
 def build_all(force: bool = False) -> None:
     build_oracle(force)
     build_gen(force)
     build_ipm(force)
     build_tools(force)
+    build_cpu_omp(force)
 
 
 if __name__ == "__main__":
