@@ -55,6 +55,16 @@ def host_cores():
         return os.cpu_count()
 
 
+def host_cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
 class Clocks:
     """Sample SM clock and throttle reasons with NVML during the timed region."""
     REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
@@ -135,7 +145,8 @@ def run_reference(args, rank, world):
             "config": {"workload": WORKLOAD, "n_total": N_TOTAL, "sample_elements_per_step": sample},
             "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": 1, "kind": "oracle",
                              "sample": f"first 2^27 elements of the C5 input per step (host array), "
-                                       f"long double Neumaier fold; host has {host_cores()} cores"},
+                                       f"long double Neumaier fold; host has {host_cores()} cores",
+                             "cpu_model": host_cpu_model()},
             "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "elements_per_s": sample / per_step, "gpu_launches": 0}
     print(json.dumps(line), file=OUT, flush=True)
@@ -161,7 +172,8 @@ def cpu_baseline_oracle(x_dev, seconds_target=10.0):
     del np
     return {"value": m * ELEM / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
             "sample": f"first {m} elements of rank 0's C5 shard (host copy), long double Neumaier fold, "
-                      f"{dt:.1f} s; host has {host_cores()} cores", "elements_per_s": m / dt}
+                      f"{dt:.1f} s; host has {host_cores()} cores", "elements_per_s": m / dt,
+            "cpu_model": host_cpu_model()}
 
 
 def cpu_native_omp(x_dev, reps=3):
@@ -186,7 +198,7 @@ def cpu_native_omp(x_dev, reps=3):
         best = dt if best is None else min(best, dt)
     return {"value": n * ELEM / best / 1e9, "unit": "GB/s", "cores": int(L.cpu_omp_threads()), "kind": "openmp",
             "sample": f"first {n} elements of rank 0's C5 shard (host copy), float32 accumulators, best of {reps}",
-            "result": float(res), "elements_per_s": n / best}
+            "result": float(res), "elements_per_s": n / best, "cpu_model": host_cpu_model()}
 
 
 def suite(ipm, torch, ipmgen, peak):
