@@ -357,6 +357,20 @@ def suite(ipm, torch, ipmgen, peak):
                     for d in (json.loads(l) for l in r.stdout.splitlines() if l.startswith("{"))}
             except (subprocess.TimeoutExpired, ValueError) as e:
                 out["library_context_cub"] = {"error": str(e)[:200]}
+    # read-only HBM roofline probe: the simplest streaming read kernel, several shapes, 8 GiB;
+    # a separate process (tools/read_probe.cu), skipped if it was not built
+    probe = os.path.join(ROOT, "tools", "bin", "read_probe")
+    if os.path.exists(probe):
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        try:
+            r = subprocess.run([probe], capture_output=True, text=True, timeout=300)
+            rows = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+            best = [d["read_probe_best_GBs"] for d in rows if "read_probe_best_GBs" in d]
+            out["read_probe"] = {"best_GBs": best[0] if best else None,
+                                 "variants": [d for d in rows if "probe" in d]}
+        except (subprocess.TimeoutExpired, ValueError) as e:
+            out["read_probe"] = {"error": str(e)[:200]}
     return out
 
 
@@ -544,6 +558,10 @@ def run_ours(args, rank, world, local_rank):
         }
         if st is not None:
             line["suite"] = st
+            rp = (st.get("read_probe") or {}).get("best_GBs")
+            if rp:  # the third denominator: the best plain streaming read measured in this run
+                line["roofline"]["read_probe_GBs"] = rp
+                line["roofline"]["frac_of_read_probe"] = achieved / rp
         print(json.dumps(line), file=OUT, flush=True)
     comm.close()
     if world > 1:

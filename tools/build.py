@@ -100,6 +100,18 @@ def build_tools(force: bool = False) -> None:
             sys.stderr.write(f"optional tool not built: {e}\n")
 
 
+def build_read_probe(force: bool = False) -> None:
+    """Read-only HBM roofline probe (tools/read_probe.cu) that bench.py runs at N = 1. Optional."""
+    out = os.path.join(ROOT, "tools", "bin", "read_probe")
+    src = os.path.join(ROOT, "tools", "read_probe.cu")
+    if force or _stale(out, [src]):
+        os.makedirs(os.path.dirname(out), exist_ok=True)
+        try:
+            _run([NVCC, *ARCH, "-O3", "-std=c++17", "-o", out, src])
+        except RuntimeError as e:
+            sys.stderr.write(f"optional tool not built: {e}\n")
+
+
 def build_cpu_omp(force: bool = False) -> None:
     """The OpenMP CPU baseline (BASELINE.md "CPU native baseline") that bench.py times at N = 1. Optional."""
     out = os.path.join(ROOT, "tools", "bin", "libcpu_omp.so")
@@ -117,6 +129,7 @@ def build_all(force: bool = False) -> None:
     build_gen(force)
     build_ipm(force)
     build_tools(force)
+    build_read_probe(force)
     build_cpu_omp(force)
 
 

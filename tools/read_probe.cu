@@ -1,0 +1,80 @@
+// read_probe.cu — read-only HBM roofline probe ("measure a read-only roofline probe"): the
+// simplest streaming read that can saturate HBM, independent of the product kernels. Each thread XOR-folds
+// 256-bit vectors (ld.global.nc.L1::no_allocate.L2::evict_first, U independent loads in flight) over a grid-stride
+// loop of an 8 GiB buffer (far above L2) and writes one word. Variants over U and resident CTAs; CUDA events,
+// median of 20 launches. Prints one JSON object per variant and a final {"read_probe_best_GBs": ...}.
+#include <cuda_runtime.h>
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <vector>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { fprintf(stderr, "CUDA %s at %d\n", cudaGetErrorString(e), __LINE__); exit(1);} } while (0)
+
+struct alignas(32) V8 { uint32_t w[8]; };
+
+__device__ __forceinline__ V8 ld256(const V8* p) {
+  V8 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.L2::256B.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v.w[0]), "=r"(v.w[1]), "=r"(v.w[2]), "=r"(v.w[3]), "=r"(v.w[4]), "=r"(v.w[5]), "=r"(v.w[6]),
+                 "=r"(v.w[7])
+               : "l"(p));
+  return v;
+}
+
+template <int U, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_read(const V8* a, int64_t nv, uint32_t* sink) {
+  const int64_t stride = (int64_t)gridDim.x * 256 * U;
+  uint32_t x = 0;
+  for (int64_t i = (int64_t)blockIdx.x * 256 * U + threadIdx.x; i < nv; i += stride) {
+    V8 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = i + u * 256 < nv ? ld256(a + i + u * 256) : V8{};
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x ^= v[u].w[k];
+  }
+  if (x == 0x9e3779b9u) sink[blockIdx.x] = x;  // practically never taken; keeps the loads alive
+}
+
+template <int U, int MINB>
+double run(const V8* a, int64_t nv, uint32_t* sink, int sms) {
+  const int grid = sms * MINB;
+  auto f = [&] { k_read<U, MINB><<<grid, 256>>>(a, nv, sink); };
+  for (int i = 0; i < 3; ++i) f();
+  CK(cudaDeviceSynchronize());
+  std::vector<float> v;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  for (int i = 0; i < 20; ++i) {
+    cudaEventRecord(e0); f(); cudaEventRecord(e1); cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1); v.push_back(ms);
+  }
+  CK(cudaGetLastError());
+  std::sort(v.begin(), v.end());
+  const double gbs = nv * 32.0 / v[v.size() / 2] / 1e6;
+  printf("{\"probe\": \"k_read\", \"U\": %d, \"ctas_per_sm\": %d, \"ms\": %.4f, \"GB/s\": %.1f}\n", U, MINB, v[v.size() / 2], gbs);
+  fflush(stdout);
+  return gbs;
+}
+
+int main() {
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  const int64_t bytes = (int64_t)8 << 30;
+  V8* a; uint32_t* sink;
+  CK(cudaMalloc(&a, bytes));
+  CK(cudaMemset(a, 0x5a, bytes));
+  CK(cudaMalloc(&sink, 1 << 20));
+  const int64_t nv = bytes / 32;
+  double best = 0;
+  best = std::max(best, run<2, 4>(a, nv, sink, sms));
+  best = std::max(best, run<4, 4>(a, nv, sink, sms));
+  best = std::max(best, run<2, 8>(a, nv, sink, sms));
+  best = std::max(best, run<4, 8>(a, nv, sink, sms));
+  best = std::max(best, run<8, 4>(a, nv, sink, sms));
+  best = std::max(best, run<4, 6>(a, nv, sink, sms));
+  printf("{\"read_probe_best_GBs\": %.1f, \"bytes\": %lld}\n", best, (long long)bytes);
+  return 0;
+}
