@@ -56,14 +56,15 @@ if __name__ == "__main__":
     if sys.argv[1] == "--child":
         child()
         sys.exit(0)
-    libs = sys.argv[1:3]
-    rounds = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+    libs = [a for a in sys.argv[1:] if not a.isdigit()]
+    rounds = next((int(a) for a in sys.argv[1:] if a.isdigit()), 3)
     res = {lib: [] for lib in libs}
     for _ in range(rounds):
         for lib in libs:
-            p = subprocess.run([sys.executable, __file__, "--child"], env=dict(os.environ, IPM_LIB=lib),
-                               capture_output=True, text=True)
+            path, *envs = lib.split("::")  # LIB::VAR=VALUE::... sets extra environment for that build's runs
+            env = dict(os.environ, IPM_LIB=path, **dict(e.split("=", 1) for e in envs))
+            p = subprocess.run([sys.executable, __file__, "--child"], env=env, capture_output=True, text=True)
             res[lib].append(json.loads(p.stdout.strip().splitlines()[-1]))
     for k in res[libs[0]][0]:
-        print(f"{k:24s} " + "  ".join(f"{os.path.basename(lib)}: " + " ".join(f"{r[k]:7.1f}" for r in res[lib])
+        print(f"{k:24s} " + "  ".join(f"{os.path.basename(lib)[:24]}: " + " ".join(f"{r[k]:7.1f}" for r in res[lib])
                                        for lib in libs) + "  GB/s")
