@@ -219,8 +219,12 @@ struct Launch {
     k_ragged_vec<R, 4, 8, 2, true, PFV><<<blocks, 128, 0, st>>>(p);  // 8 CTAs x 4 warps per SM, 2 vectors per lane
     k_ragged_fix<R><<<(unsigned)((nw + 7) / 8), 256, 0, st>>>(p, nw);
   }
-  static void two_d(const Params2D& q, int grid, cudaStream_t st) {
-    k_2d<R, FLAT_BLOCK, 4><<<grid, FLAT_BLOCK, 0, st>>>(q);
+  // 8-byte folds run 3 CTAs x 256 per SM with up to 85 registers (+1-3 % over 4 CTAs at 64 registers; 4-byte folds
+  // lose up to 17 % that way, profiles/r01_ab_2d_minb.txt). max_grid = SMs x the resident CTAs per SM.
+  static constexpr int TWO_D_MINB = sizeof(typename R::B) == 8 ? 3 : 4;
+  static void two_d(const Params2D& q, int max_items_grid, int sms, cudaStream_t st) {
+    const int grid = std::max(1, std::min(max_items_grid, sms * TWO_D_MINB));
+    k_2d<R, FLAT_BLOCK, 4, 0, TWO_D_MINB><<<grid, FLAT_BLOCK, 0, st>>>(q);
   }
   static cudaError_t seg_tma(const SegParams& p, int grid, cudaStream_t st) {
     constexpr int smem = SegTma<R, TMA_WARPS, TMA_S, TMA_CH>::SMEM;
@@ -249,7 +253,7 @@ struct Launch {
 
 struct Table {
   void (*flat)(const FlatParams&, dim3, cudaStream_t);
-  void (*two_d)(const Params2D&, int, cudaStream_t);
+  void (*two_d)(const Params2D&, int, int, cudaStream_t);  // (params, grid bound by the items, SM count, stream)
   void (*ragged)(const RaggedParams&, int, int64_t, cudaStream_t);
   void (*seg_warp)(const SegParams&, int, cudaStream_t);  // (params, SM count, stream)
   cudaError_t (*seg_tma)(const SegParams&, int, cudaStream_t);
@@ -872,11 +876,10 @@ ipm_status ipm_reduce_2d_async(ipm_op op, ipm_dtype dt, const void* dev, int64_t
   const int64_t vw = 32 / (int64_t)esize(dt), chv = 32 * 4;
   const int64_t per_row = std::max<int64_t>(1, (cols / vw + chv - 1) / chv);
   const int64_t items = rows * per_row;
-  const int64_t grid = std::max<int64_t>(
-      1, std::min<int64_t>((int64_t)sm_count() * flat_ctas_per_sm(), (items + FLAT_BLOCK / 32 - 1) / (FLAT_BLOCK / 32)));
+  const int64_t item_grid = std::min<int64_t>(INT32_MAX, (items + FLAT_BLOCK / 32 - 1) / (FLAT_BLOCK / 32));
   {
     ProfScope ps(st, 3);
-    table(op, dt)->two_d(q, (int)grid, st);
+    table(op, dt)->two_d(q, (int)item_grid, sm_count(), st);
   }
   CK(cudaGetLastError());
   return IPM_OK;

@@ -536,8 +536,8 @@ struct Params2D {
   FlatParams f;   // f.a = base, f.n unused
   int64_t rows, cols, row_stride;
 };
-template <class R, int BLOCK, int U, int PF = 0>
-__global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_2d(Params2D q) {
+template <class R, int BLOCK, int U, int PF = 0, int MINB = 1024 / BLOCK>
+__global__ void __launch_bounds__(BLOCK, MINB) k_2d(Params2D q) {
   using B = typename R::B;
   using A = typename R::A;
   using VT = typename Vec<B>::T;
