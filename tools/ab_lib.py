@@ -12,7 +12,9 @@ CASES = [("flat", "float32", "+", 1 << 28), ("flat", "float64", "max", 1 << 28),
          ("2d", "float64", "+", 16384 * 16384), ("seg", "float32", "max", 65536 * 4096),
          ("seg", "float64", "+", 65536 * 4096), ("seg", "int32", "^", 65536 * 4096), ("seg", "int64", "min", 65536 * 4096),
          ("2d", "int32", "+", 16384 * 16384), ("2d", "int64", "+", 8192 * 16384), ("2d", "int64", "max", 8192 * 16384),
-         ("2d", "float64", "max", 8192 * 16384), ("2d", "float32", "&&", 16384 * 16384), ("2d", "int32", "*", 16384 * 16384)]
+         ("2d", "float64", "max", 8192 * 16384), ("2d", "float32", "&&", 16384 * 16384), ("2d", "int32", "*", 16384 * 16384),
+         ("flat", "float64", "+", 1 << 28), ("flat", "float64", "min", 1 << 28), ("flat", "int64", "max", 1 << 30),
+         ("flat", "int64", "*", 1 << 30), ("flat", "float32", "max", 1 << 28)]
 if os.environ.get("AB_CASES"):  # e.g. AB_CASES=2d: only cases of that kind
     CASES = [c for c in CASES if c[0] in os.environ["AB_CASES"].split(",")]
 
