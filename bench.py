@@ -2,6 +2,9 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--no-suite] [--no-e2e]
     torchrun --nproc-per-node N bench.py --gpus N ...        (one process per GPU, NCCL)
+    python bench.py --gpus N ...   without a launcher re-launches itself under torch.distributed.run (N ranks);
+                                   under a launcher WORLD_SIZE must equal --gpus (else exit 2)
+    python bench.py --gpus N --dry-run   the N-rank wiring on CPU (gloo): shards, id bootstrap, path decision
 
 One step = one execution of the clause over the whole 2^34-element iteration space: every rank runs the flat
 reduction kernel over its contiguous shard (rows a1-a6 of SURVEY.md §8(a)); the kernel's last CTA exchanges the
@@ -14,7 +17,10 @@ flush is needed between steps. Timed with CUDA events between two barriers, max 
 Rank 0 prints ONE JSON line. Besides the contract keys it carries:
   roofline      the flat kernel's HBM roofline: algorithmic bytes per launch / its live per-launch event time
   cpu_baseline  the CPU oracle (test infrastructure, tests/ + here only) timed on a bounded sample, 1 core
-  e2e           the same metric through ipm_reduce_host_dist: pinned host shards -> devices + the rank exchange
+  e2e           the same metric through ipm_reduce_host_dist: pinned host shards -> devices + the rank exchange,
+                with the box's plain pinned H2D bandwidth as its roofline
+  result_check  the timed steps' result against the oracle's fold of the whole 2^34-element input (host cores)
+  per_gpu       `value` is the whole-job aggregate (bench contract); the metric's per-GPU figures are here
   suite         (N=1) the other BASELINE configs device-timed: C1 latency, C2 per op, C3 segmented, C4 per op,
                 the NEXT rows (fused, 2-D, ragged), and torch / CUB reductions on the same shapes as context
 `--impl reference` times the CPU oracle as the reference arm on the same metric (no GPU work).
@@ -374,6 +380,91 @@ def suite(ipm, torch, ipmgen, peak):
     return out
 
 
+def all_ranks_ok(local_bad: int, world: int, device) -> bool:
+    """Every rank must take the same exchange path: True iff no rank reported a problem (MAX all-reduce of the
+    per-rank flags; gloo on CPU in --dry-run, NCCL on the GPUs)."""
+    import torch
+    import torch.distributed as dist
+    bad = torch.tensor([int(local_bad)], device=device)
+    if world > 1:
+        dist.all_reduce(bad, op=dist.ReduceOp.MAX)
+    return int(bad.item()) == 0
+
+
+def shard_partition_ok(ipm, world, rank):
+    """This rank's contiguous shard of the C5 iteration space, and whether all ranks' shards tile [0, N) exactly."""
+    import torch.distributed as dist
+    lo, hi = ipm.shard_range(N_TOTAL, rank, world)
+    shards = [(lo, hi)]
+    if world > 1:
+        shards = [None] * world
+        dist.all_gather_object(shards, (lo, hi))
+    ok = shards[0][0] == 0 and shards[-1][1] == N_TOTAL and all(
+        a[1] == b[0] and a[0] <= a[1] for a, b in zip(shards, shards[1:]))
+    return lo, hi, shards, ok
+
+
+def run_dry(args, rank, world):
+    """--dry-run: the N-rank wiring of the ours arm WITHOUT a GPU (gloo on CPU): shard plan, the NCCL-id bootstrap
+    through the torch.distributed store, the fused-probe fallback decision. No kernel runs; the line says so."""
+    import torch.distributed as dist
+
+    from paper_1412_1127_b200 import ipm
+    if world > 1:
+        dist.init_process_group("gloo")
+        store = dist.distributed_c10d._get_default_store()
+    else:
+        store = dist.HashStore()
+    lo, hi, shards, part_ok = shard_partition_ok(ipm, world, rank)
+    try:
+        uid = ipm.Comm.bootstrap_id(rank, store, key="bench_dry_id")
+        id_src = "ncclGetUniqueId"
+    except ipm.IpmError:  # no usable network interface for NCCL's id on this host: the store path still runs
+        if rank == 0:
+            store.set("bench_dry_id", os.urandom(ipm.lib.ipm_comm_id_bytes()))
+        uid = store.get("bench_dry_id")
+        id_src = "random bytes (ncclGetUniqueId unavailable)"
+    ids = [uid]
+    if world > 1:
+        ids = [None] * world
+        dist.all_gather_object(ids, uid)
+    # the fused-exchange probe: a rank whose probe failed (simulated by --dry-run-fail-rank) switches ALL ranks
+    fused = all_ranks_ok(int(rank == args.dry_run_fail_rank), world, "cpu")
+    paths = [fused]
+    if world > 1:
+        paths = [None] * world
+        dist.all_gather_object(paths, fused)
+    if rank == 0:
+        line = {"metric": METRIC, "value": None, "unit": "GB/s", "n_gpus": world, "gpus_requested": args.gpus,
+                "dry_run": True, "note": "wiring only (gloo on CPU): no GPU, no kernel, no timing",
+                "shards": shards, "shards_partition": part_ok, "id_agree": all(i == ids[0] for i in ids),
+                "id_source": id_src, "exchange": "fused peer-memory" if fused else "ncclAllGather+fold",
+                "ranks_same_path": all(p == paths[0] for p in paths)}
+        print(json.dumps(line), file=OUT, flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def result_check(result, threads=None):
+    """The oracle's answer for the WHOLE C5 input (2^34 elements): the plain compensated left fold, generated and
+    folded on the host cores in 256 contiguous pieces merged in piece order (oracle.reduce_spec_split, SURVEY.md
+    §8(d)); part of the CPU-baseline leg (the oracle's one use here besides cpu_baseline and the reference arm)."""
+    import numpy as np
+
+    import ipmgen
+    import oracle
+    t0 = time.perf_counter()
+    want_t, want_ld, used = oracle.reduce_spec_split("+", ipmgen.Spec("float32", N_TOTAL, "random", seed=1),
+                                                     pieces=256, threads=threads)
+    dt = time.perf_counter() - t0
+    rel = abs(float(np.longdouble(result) - want_ld)) / float(want_ld)
+    return {"gpu": float(result), "oracle_ld": float(want_ld), "oracle_f32": float(want_t), "rel_err": rel,
+            "tol": 1e-5, "ok": rel <= 1e-5, "bits_equal": bool(np.float32(result) == want_t),
+            "oracle_seconds": dt, "oracle_threads": used,
+            "how": "oracle.reduce_spec_split: 256 contiguous pieces of the generated C5 input, compensated long "
+                   "double folds on the host cores, merged in piece order"}
+
+
 def ctypes_err(ipm, comm):
     import ctypes
     e = ctypes.c_int(0)
@@ -398,7 +489,8 @@ def run_ours(args, rank, world, local_rank):
         store = dist.HashStore()
     peak, peak_src = peaks()
 
-    lo, hi = ipm.shard_range(N_TOTAL, rank, world)
+    lo, hi, _, part_ok = shard_partition_ok(ipm, world, rank)
+    assert part_ok, "the ranks' shards do not tile the iteration space"
     n_shard = hi - lo
     spec = ipmgen.Spec("float32", N_TOTAL, "random", seed=1)
     x = torch.empty(n_shard, dtype=torch.float32, device="cuda")
@@ -412,10 +504,9 @@ def run_ours(args, rank, world, local_rank):
         probe = torch.ones(1024, dtype=torch.float32, device="cuda")
         got = comm.reduce_async("+", probe).cpu().numpy()[0]
         err = ctypes_err(ipm, comm)
-        bad = torch.tensor([int(err or got != 1024.0 * world)], device="cuda")
-        dist.all_reduce(bad, op=dist.ReduceOp.MAX)
+        ok = all_ranks_ok(int(err or got != 1024.0 * world), world, "cuda")
         ipm.set_option("dist_timeout_ms", 30000)
-        if bad.item():
+        if not ok:
             ipm.set_option("dist_mode", "nccl")
             comm_fused = False
     ws = ipm.workspace()
@@ -480,6 +571,18 @@ def run_ours(args, rank, world, local_rank):
             host.copy_(x)
             del x
             torch.cuda.empty_cache()
+            # the e2e roofline: plain pinned host -> device copy bandwidth of this box (1 GiB cudaMemcpyAsync)
+            pn = min(n_shard, 1 << 28)
+            dbuf = torch.empty(pn, dtype=torch.float32, device="cuda")
+            dbuf.copy_(host[:pn], non_blocking=True)
+            h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            h0.record(stream)
+            for _ in range(3):
+                dbuf.copy_(host[:pn], non_blocking=True)
+            h1.record(stream)
+            h1.synchronize()
+            h2d_gbs = 3 * pn * ELEM / (h0.elapsed_time(h1) / 1e3) / 1e9
+            del dbuf
             for _ in range(1):
                 comm.reduce_host("+", host, init=init, ws=ws)  # warm (allocates the staging buffers)
             barrier()
@@ -498,7 +601,11 @@ def run_ours(args, rank, world, local_rank):
                    "h2d_bytes_per_step": total_bytes, "d2h_bytes_per_step": 4 * world, "steps": e2e_steps,
                    "ms_per_step": float(e_ms.item()), "path": "ipm_reduce_host_dist: pinned host shard per rank, 64 MiB "
                    "chunks double-buffered H2D overlapped with the reduce kernels, then the rank exchange",
-                   "host_result_rank0": float(part)}
+                   "host_result_rank0": float(part),
+                   "h2d_probe_GBs_per_gpu": h2d_gbs,
+                   "frac_of_h2d": total_bytes / (float(e_ms.item()) / 1e3) / 1e9 / (h2d_gbs * world),
+                   "h2d_probe": "1 GiB pinned host -> device cudaMemcpyAsync, 3 reps, same process, before the e2e "
+                                "steps; frac_of_h2d = e2e value / (probe x n_gpus)"}
             del host
             ipm.lib.ipm_release_staging()
         except Exception as ex:  # pinned allocation can fail on small hosts: say so, keep the device number
@@ -520,6 +627,13 @@ def run_ours(args, rank, world, local_rank):
             except Exception as ex:  # a baseline only: never fail the bench line over it
                 cpu_omp = {"value": None, "unit": "GB/s", "kind": "openmp", "error": repr(ex)[:200]}
             del xs
+        # the oracle's answer for the whole 2^34 input against the timed steps' result (same on every rank)
+        rcheck = None
+        if not args.no_check:
+            try:
+                rcheck = result_check(result)
+            except Exception as ex:  # the check must not hide the measurement; report why it did not run
+                rcheck = {"ok": None, "error": repr(ex)[:200]}
         st = suite(ipm, torch, ipmgen, peak) if (world == 1 and not args.no_suite) else None
         traffic = None
         tp = os.path.join(ROOT, "profiles", "r01_traffic.json")
@@ -538,6 +652,10 @@ def run_ours(args, rank, world, local_rank):
                        "parallelism": f"shard{world}+" + ("fused peer-memory exchange in the reduction kernel"
                                                           if comm_fused else "ncclAllGather(8B/rank)+fold kernel"),
                        "l2": "inputs larger than L2 (64/N GiB per GPU): no flush needed"},
+            "value_scope": "aggregate over all n_gpus (bench contract); per-GPU figures under per_gpu",
+            "per_gpu": {"value": value / world, "unit": "GB/s", "pct_of_hbm_peak": 100.0 * value / world / peak,
+                        "pct_of_8TBs": 100.0 * value / world / 8000.0, "elements_per_s": N_TOTAL / world /
+                        (ms_step / 1e3)},
             "per_gpu_GBs": value / world, "pct_of_hbm_peak": 100.0 * value / world / peak,
             "elements_per_s": N_TOTAL / (ms_step / 1e3),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -554,7 +672,7 @@ def run_ours(args, rank, world, local_rank):
                                   if comm_fused else "per step: 1 k_flat_guided + 1 k_finalize (plus NCCL's own "
                                   "AllGather kernel)"),
             "clocks": clk.summary(), "result_rank0": result, "spinup_steps": spin,
-            "ranks_agree": ranks_agree,
+            "ranks_agree": ranks_agree, "result_check": rcheck,
         }
         if st is not None:
             line["suite"] = st
@@ -566,6 +684,19 @@ def run_ours(args, rank, world, local_rank):
     comm.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def spawn_ranks(n: int) -> int:
+    """`python bench.py --gpus N` without torchrun: relaunch this command under torch.distributed.run with N
+    processes on this node (127.0.0.1 rendezvous); rank 0's JSON line goes to our stdout."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    print("bench.py: launching " + " ".join(cmd), file=sys.stderr, flush=True)
+    return subprocess.run(cmd, stdout=OUT.fileno(), stderr=sys.stderr.fileno()).returncode
 
 
 def _claim_stdout():
@@ -591,10 +722,23 @@ def main():
     ap.add_argument("--no-suite", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-check", action="store_true", help="skip the whole-input oracle check of the C5 result")
+    ap.add_argument("--dry-run", action="store_true", help="N-rank wiring on CPU (gloo), no GPU work")
+    ap.add_argument("--dry-run-fail-rank", type=int, default=-1, help="--dry-run: this rank's exchange probe fails")
     args = ap.parse_args()
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args.gpus))       # no launcher: start one process per GPU ourselves
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but the launcher started WORLD_SIZE={world} ranks", file=sys.stderr)
+        sys.exit(2)
+    if args.dry_run:
+        run_dry(args, rank, world)
+        return
     if args.impl == "reference":
         run_reference(args, rank, world)
         return

@@ -133,8 +133,9 @@ ipm_status ipm_reduce_async(ipm_op op, ipm_dtype dt, const void* dev, int64_t n,
  *   for r in [0, rows): dev_out[r] = init ⊕ fold_{j<cols} dev[r*row_stride + j]
  * dev: device array, row-major, row_stride >= cols elements between row starts (any alignment to the
  * element size). init: host scalar (NULL = identity). dev_out: rows elements of dt, device. Asynchronous
- * (stream order). workspace may be NULL unless rows < the SM count and cols is large, in which case rows
- * are split across CTAs and a workspace (as above) is required (IPM_E_WORKSPACE otherwise). */
+ * (stream order). workspace may be NULL unless rows < 2 x the SM count and cols >= 2048 x (32 / element size)
+ * elements, in which case each row is split across several CTAs and a workspace (as above) is required
+ * (IPM_E_WORKSPACE otherwise). Passing a workspace always is safe. */
 ipm_status ipm_reduce_segmented(ipm_op op, ipm_dtype dt, const void* dev, int64_t rows, int64_t cols,
                                 int64_t row_stride, const void* init, void* dev_out, void* workspace,
                                 void* stream);
@@ -196,7 +197,10 @@ ipm_status ipm_reduce_ragged(ipm_op op, ipm_dtype dt, const void* dev, const int
  * array is streamed to the device in chunks through two library-owned staging buffers (allocated once
  * through the allocator hook and kept until ipm_release_staging), each chunk's H2D copy overlapping the
  * reduction of the previous chunk; partial results stay on the device; one 8-byte D2H at the end.
- * Pinned host memory is fastest; pageable memory works. Blocks until *inout holds the result. */
+ * Pinned host memory is fastest; pageable memory works. Blocks until *inout holds the result.
+ * Thread safety: concurrent calls from several host threads on different streams (each with its own workspace)
+ * are safe — they share the staging buffers, and a call's copies into a buffer wait for the previous caller's
+ * last kernel that read it (so concurrent host-path calls partly serialise on the two buffers). */
 ipm_status ipm_reduce_host(ipm_op op, ipm_dtype dt, const void* host, int64_t n, void* inout, void* workspace,
                            void* stream);
 ipm_status ipm_release_staging(void);
@@ -235,6 +239,17 @@ ipm_status ipm_set_option(ipm_option key, int64_t value);
 
 /* Launch geometry the library uses for a flat reduce of n elements (for tests and the roofline report). */
 ipm_status ipm_flat_geometry(ipm_dtype dt, int64_t n, int* grid, int* block);
+/* Which flat kernel ipm_reduce / ipm_reduce_async would launch for n elements of dt under the current options
+ * (the same decision function the launch uses): 0 static grid-stride tiles (inputs <= 64 MiB, or
+ * IPM_OPT_DETERMINISTIC = 2), 1 the guided deterministic schedule (k_flat_guided, the default above 64 MiB),
+ * 2 purely dynamic tiles (IPM_OPT_DETERMINISTIC = 0), -1 no reduction kernel (n == 0). For tests that must
+ * know which schedule they exercised. */
+ipm_status ipm_flat_schedule(ipm_dtype dt, int64_t n, int* schedule);
+/* The identity of op on dt as one element of dt ("per-thread private v initialized to op's
+ * identity"): 0 for + | ^ ||; 1 (1.0) for * &&; the type's minimum (-inf) for max, maximum (+inf) for min; all
+ * bits set for &. init = identity makes init ⊕ fold == fold, so a caller of the synchronous calls (whose `inout`
+ * always carries an original value) passes this when the variable has none. IPM_E_REDOP for an illegal pair. */
+ipm_status ipm_identity(ipm_op op, ipm_dtype dt, void* out);
 
 /* ------------------------------------------------------------------ multi-GPU (one process per GPU)
  * The iteration space is sharded contiguously: rank r owns [r*n/P, (r+1)*n/P) (floor division, 128-bit

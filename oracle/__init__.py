@@ -40,6 +40,8 @@ def lib():
         L.ora_fold.restype = None
         L.ora_result.argtypes = [vp, vp, vp]
         L.ora_result.restype = None
+        L.ora_merge.argtypes = [vp, vp]
+        L.ora_merge.restype = ci
         L.ora_reduce.argtypes = [ci, ci, vp, i64, vp, vp, vp]
         L.ora_reduce.restype = ci
         L.ora_reduce_segmented.argtypes = [ci, ci, vp, i64, i64, i64, vp, vp, vp]
@@ -81,6 +83,12 @@ class Fold:
             lib().ora_fold(self._st, a.ctypes.data, a.size)
         return self
 
+    def merge(self, later: "Fold") -> "Fold":
+        """Continue this fold with the fold of the NEXT contiguous chunk (begun without init): ora_merge."""
+        if lib().ora_merge(self._st, later._st):
+            raise ValueError("merge of folds of different op / dtype")
+        return self
+
     def result(self):
         """(value as a numpy scalar of the element type, the oracle's long double value)."""
         out = np.zeros(1, dtype=NP[self.dtype])
@@ -103,6 +111,37 @@ def reduce_spec(op: str, spec, init=None, lo: int = 0, hi: int | None = None, ch
     for c in ipmgen.chunks(spec, chunk, lo, hi):
         f.fold(c)
     return f.result()
+
+
+def reduce_spec_split(op: str, spec, init=None, lo: int = 0, hi: int | None = None, pieces: int = 64,
+                      threads: int | None = None, chunk: int = 1 << 22):
+    """reduce_spec over [lo, hi) split into `pieces` contiguous pieces folded on `threads` host threads (each piece
+    a plain left fold of generated chunks), then merged in piece order (ora_merge) — SURVEY.md §8(d)'s permitted
+    split of the C5 oracle. Returns (T value, long double value, threads used)."""
+    import concurrent.futures as cf
+    hi = spec.n if hi is None else hi
+    pieces = max(1, min(pieces, hi - lo)) if hi > lo else 1
+    if threads is None:
+        try:
+            threads = len(os.sched_getaffinity(0))
+        except Exception:
+            threads = os.cpu_count() or 1
+    bounds = [lo + (hi - lo) * k // pieces for k in range(pieces + 1)]
+
+    def piece(k):
+        f = Fold(op, spec.dtype, init if k == 0 else None)
+        import ipmgen
+        for c in ipmgen.chunks(spec, chunk, bounds[k], bounds[k + 1]):
+            f.fold(c)   # ctypes releases the GIL: the pieces run in parallel
+        return f
+
+    with cf.ThreadPoolExecutor(max_workers=threads) as ex:
+        folds = list(ex.map(piece, range(pieces)))
+    total = folds[0]
+    for f in folds[1:]:
+        total.merge(f)
+    v, ld = total.result()
+    return v, ld, threads
 
 
 def reduce_segmented(op: str, a, rows: int, cols: int, stride: int | None = None, dtype: str | None = None,

@@ -202,6 +202,29 @@ void ora_result(const ora_state* st, void* out, long double* out_ld) {
   if (out_ld) *out_ld = v;
 }
 
+/* Split fold (the C5 oracle may "split into P contiguous chunks on P host threads, combined
+ * in chunk order in long double"). dst = the fold of chunk 0 (begun from the original value, R1), src = the
+ * fold of the next contiguous chunk (begun from the identity, no init). Merging in chunk order continues the
+ * left fold with src's running value as ONE more operand: for the exact ops (integer, bitwise, logical,
+ * max/min) this is the same result as one unsplit fold (associativity); for float + both long double words of
+ * src's compensated sum are folded through the same Neumaier step (so the error stays ~2u_ld per chunk); for
+ * float * src's long double product is multiplied in. */
+int ora_merge(ora_state* dst, const ora_state* src) {
+  if (dst->op != src->op || dst->dt != src->dt) return 1;
+  if (!is_float(dst->dt)) {
+    fold_int(dst, src->r);          /* src->r is the running w-bit word (0/1 for && ||) */
+  } else {
+    switch (dst->op) {
+      case O_ADD: fold_flt(dst, src->s); fold_flt(dst, src->c); dst->count--; break;
+      case O_MUL: fold_flt(dst, src->s); break;
+      case O_MAX: case O_MIN: fold_flt(dst, (long double)src->m); break;
+      case O_LAND: case O_LOR: fold_flt(dst, src->r ? 1.0L : 0.0L); break;
+    }
+  }
+  dst->count += src->count - 1;
+  return 0;
+}
+
 /* flat clause: var = init ⊕ fold(a[0..n)) */
 int ora_reduce(int op, int dt, const void* a, int64_t n, const void* init, void* out, long double* out_ld) {
   ora_state st;

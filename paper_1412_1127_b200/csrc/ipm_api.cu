@@ -180,23 +180,29 @@ long long dist_timeout_ns() { return g_opt_dist_timeout_ms.load(std::memory_orde
   X(IPM_ADD, IPM_F64) X(IPM_MUL, IPM_F64) X(IPM_MAX, IPM_F64) X(IPM_MIN, IPM_F64) X(IPM_LAND, IPM_F64)     \
   X(IPM_LOR, IPM_F64)
 
+// Which flat kernel a launch takes (the one decision both Launch::flat and ipm_flat_schedule use). The flat
+// clause uses the guided schedule (k_flat_guided: ~90% of the tiles static, the rest in chunks claimed
+// dynamically, one partial slot per element range) — load-balanced and bit-reproducible for every operator.
+// IPM_OPT_DETERMINISTIC = 0 selects the purely dynamic tile schedule instead (float + and * may then differ in
+// the last bits between runs). Multi-row launches (grid.y > 1), the per-block partials mode and inputs up to
+// 64 MiB (latency-bound: the static schedule saves the chunk claims, C1: 12.4 -> 10.3 us) keep the static
+// grid-stride schedule.
+enum { SCHED_STATIC = 0, SCHED_GUIDED = 1, SCHED_DYNAMIC = 2 };
+static int flat_schedule(size_t es, int64_t n, unsigned grid_x, unsigned grid_y, bool has_counter) {
+  const bool small = n * (int64_t)es <= (64ll << 20);
+  const int det = g_opt_deterministic.load(std::memory_order_relaxed);
+  if (has_counter && grid_y == 1 && grid_x > 1 && det != 2 && !small) return det ? SCHED_GUIDED : SCHED_DYNAMIC;
+  return SCHED_STATIC;
+}
+
 template <int OP, int DT>
 struct Launch {
   using R = Red<OP, DT>;
-  // the flat clause uses the guided schedule (k_flat_guided: ~90% of the tiles static, the rest in chunks
-  // claimed dynamically, one partial slot per element range) — load-balanced and bit-reproducible for every
-  // operator. IPM_OPT_DETERMINISTIC = 0 selects the purely dynamic tile schedule instead (float + and * may
-  // then differ in the last bits between runs). Multi-row launches (grid.y > 1) and the per-block partials
-  // mode keep the static grid-stride schedule.
   static void flat(const FlatParams& p, dim3 grid, cudaStream_t st) {
-    // up to 64 MiB the launch is latency-bound: the static schedule saves the chunk claims (C1: 12.4 -> 10.3 us)
-    const bool small = p.n * (int64_t)sizeof(typename R::B) <= (64ll << 20);
-    const int det = g_opt_deterministic.load(std::memory_order_relaxed);
-    if (p.counter && grid.y == 1 && grid.x > 1 && det != 2 && !small) {
-      if (det) k_flat_guided<R, FLAT_BLOCK, GUIDED_U, true><<<grid, FLAT_BLOCK, 0, st>>>(p);
-      else k_flat<R, FLAT_BLOCK, FLAT_U, 0, 2><<<grid, FLAT_BLOCK, 0, st>>>(p);
-    } else {
-      k_flat<R, FLAT_BLOCK, FLAT_U, 0, 0><<<grid, FLAT_BLOCK, 0, st>>>(p);
+    switch (flat_schedule(sizeof(typename R::B), p.n, grid.x, grid.y, p.counter != nullptr)) {
+      case SCHED_GUIDED: k_flat_guided<R, FLAT_BLOCK, GUIDED_U, true><<<grid, FLAT_BLOCK, 0, st>>>(p); break;
+      case SCHED_DYNAMIC: k_flat<R, FLAT_BLOCK, FLAT_U, 0, 2><<<grid, FLAT_BLOCK, 0, st>>>(p); break;
+      default: k_flat<R, FLAT_BLOCK, FLAT_U, 0, 0><<<grid, FLAT_BLOCK, 0, st>>>(p); break;
     }
   }
   static void seg_warp(const SegParams& p, int sms, cudaStream_t st) {
@@ -431,6 +437,7 @@ static ipm_status release_staging_locked() {
   for (int i = 0; i < 2; ++i) {
     if (g_stage.buf[i]) {
       cudaStreamSynchronize(g_stage.copy);
+      if (g_stage.consumed[i]) cudaEventSynchronize(g_stage.consumed[i]);  // the last reader (any caller's stream)
       dev_free(g_stage.buf[i], g_stage.copy);
       g_stage.buf[i] = nullptr;
     }
@@ -604,6 +611,42 @@ ipm_status ipm_flat_geometry(ipm_dtype dt, int64_t n, int* grid, int* block) {
   if (n < 0) return IPM_E_SIZE;
   if (grid) *grid = (int)flat_grid(dt, n);
   if (block) *block = FLAT_BLOCK;
+  return IPM_OK;
+}
+
+ipm_status ipm_flat_schedule(ipm_dtype dt, int64_t n, int* schedule) {
+  if (!esize(dt)) return IPM_E_DTYPE;
+  if (n < 0) return IPM_E_SIZE;
+  if (!schedule) return IPM_E_NULL;
+  *schedule = n == 0 ? -1 : flat_schedule(esize(dt), n, (unsigned)flat_grid(dt, n), 1, true);
+  return IPM_OK;
+}
+
+// identities of the nine operators ("per-thread private v initialized to op's identity"; DESIGN.md
+// R2: -inf / +inf for float max / min) as element bits; the device-side Red<>::id() of the kernels agrees with
+// it (tests/test_gpu_parity.py: the n = 0 finalize kernel writes exactly these bits)
+ipm_status ipm_identity(ipm_op op, ipm_dtype dt, void* out) {
+  ipm_status s;
+  if ((s = validate(op, dt))) return s;
+  if (!out) {
+    set_error("NULL out");
+    return IPM_E_NULL;
+  }
+  const bool w4 = esize(dt) == 4, fl = dt == IPM_F32 || dt == IPM_F64;
+  uint64_t b = 0;
+  switch (op) {
+    case IPM_ADD: case IPM_BOR: case IPM_BXOR: case IPM_LOR: b = 0; break;
+    case IPM_MUL: case IPM_LAND: b = fl ? (w4 ? 0x3F800000ull : 0x3FF0000000000000ull) : 1ull; break;
+    case IPM_MAX: b = fl ? (w4 ? 0xFF800000ull : 0xFFF0000000000000ull) : (w4 ? 0x80000000ull : 1ull << 63); break;
+    case IPM_MIN: b = fl ? (w4 ? 0x7F800000ull : 0x7FF0000000000000ull) : (w4 ? 0x7FFFFFFFull : ~0ull >> 1); break;
+    case IPM_BAND: b = w4 ? 0xFFFFFFFFull : ~0ull; break;
+  }
+  if (w4) {
+    const uint32_t u = (uint32_t)b;
+    memcpy(out, &u, 4);
+  } else {
+    memcpy(out, &b, 8);
+  }
   return IPM_OK;
 }
 
@@ -1001,8 +1044,14 @@ ipm_status stream_host_partial(ipm_op op, ipm_dtype dt, const void* host, int64_
     g_stage.device = dev;
   }
   const int64_t per = (int64_t)(chunk_bytes / es);
-  // the staging buffers are free once everything previously queued on `st` has run
-  for (int i = 0; i < 2; ++i) CK(cudaEventRecord(g_stage.consumed[i], st));
+  // The staging buffers are shared by every caller (the lock covers enqueueing only, not execution): a buffer is
+  // free once the previous caller's last kernel that read it has run (consumed[i], recorded on THAT caller's
+  // stream) and everything queued earlier on `st` has run. `st` waits for the former, then consumed[i] is
+  // re-recorded on `st` so the copies below wait for both.
+  for (int i = 0; i < 2; ++i) {
+    CK(cudaStreamWaitEvent(st, g_stage.consumed[i], 0));
+    CK(cudaEventRecord(g_stage.consumed[i], st));
+  }
   int64_t c = 0;
   for (int64_t off = 0; off < n; off += per, ++c) {
     const int b = (int)(c & 1);

@@ -7,6 +7,7 @@ There is no fallback: if ``libipm.so`` is missing or fails to load, importing th
 from __future__ import annotations
 
 import ctypes
+import functools
 import os
 import threading
 
@@ -73,6 +74,8 @@ def _load():
         "ipm_profile_read": ([vp, vp, ci, ctypes.POINTER(ci)], ci),
         "ipm_profile_disable": ([], ci),
         "ipm_flat_geometry": ([ci, i64, ctypes.POINTER(ci), ctypes.POINTER(ci)], ci),
+        "ipm_flat_schedule": ([ci, i64, ctypes.POINTER(ci)], ci),
+        "ipm_identity": ([ci, ci, vp], ci),
         "ipm_comm_id_bytes": ([], sz),
         "ipm_comm_unique_id": ([vp], ci),
         "ipm_comm_init": ([ctypes.POINTER(vp), ci, ci, vp, ci], ci),
@@ -100,7 +103,7 @@ EXPORTED = ("ipm_status_str ipm_last_error_message ipm_op_legal ipm_dtype_size i
             "ipm_copyin ipm_create ipm_present ipm_update_device ipm_update_host ipm_copyout ipm_delete "
             "ipm_present_count ipm_workspace_bytes ipm_workspace_init ipm_reduce ipm_reduce_async "
             "ipm_reduce_segmented ipm_reduce_ragged ipm_reduce_partials ipm_finalize_partials ipm_reduce_2d ipm_reduce_2d_async ipm_fused_nvars ipm_reduce_fused ipm_reduce_fused_async ipm_reduce_host ipm_release_staging ipm_set_option ipm_profile_enable ipm_profile_read "
-            "ipm_profile_disable ipm_flat_geometry ipm_comm_id_bytes "
+            "ipm_profile_disable ipm_flat_geometry ipm_flat_schedule ipm_identity ipm_comm_id_bytes "
             "ipm_comm_unique_id ipm_comm_init ipm_comm_destroy ipm_comm_init_group ipm_comm_ipc_handle_bytes "
             "ipm_comm_create_ipc ipm_comm_attach_ipc ipm_shard_range ipm_comm_uses_peer_memory ipm_comm_error "
             "ipm_reduce_host_dist ipm_reduce_dist "
@@ -199,9 +202,36 @@ def workspace(stream=None, device=None) -> torch.Tensor:
     with _ws_lock:
         ws = _ws_cache.get((dev, s))
         if ws is None:
-            ws = torch.zeros(WS_BYTES, dtype=torch.uint8, device=f"cuda:{dev}")
+            ws = torch.empty(WS_BYTES, dtype=torch.uint8, device=f"cuda:{dev}")
+            # zeroed ON the stream the library will use it on (ipm_workspace_init), so the first kernel's
+            # tickets and counter cannot race with a memset queued on another stream
+            with torch.cuda.device(dev):
+                _check(lib.ipm_workspace_init(ws.data_ptr(), s), "ipm_workspace_init")
             _ws_cache[(dev, s)] = ws
     return ws
+
+
+def _check_out(out: torch.Tensor, like: torch.Tensor, count: int, what: str = "out") -> None:
+    """A caller-supplied result tensor must match the input's dtype and device, be contiguous and hold at least
+    `count` elements (the library writes count elements of the input's type there)."""
+    if not out.is_cuda or out.device != like.device:
+        raise ValueError(f"{what} must be a CUDA tensor on {like.device}")
+    if out.dtype != like.dtype:
+        raise ValueError(f"{what} has dtype {out.dtype}, expected {like.dtype}")
+    if not out.is_contiguous() or out.numel() < count:
+        raise ValueError(f"{what} must be contiguous with at least {count} elements")
+
+
+def _check_region(t: torch.Tensor, rows: int, cols: int, row_stride: int) -> None:
+    """rows x cols elements at row_stride must lie inside t's storage from t's first element"""
+    if rows < 0 or cols < 0 or row_stride < cols:
+        raise ValueError("need rows >= 0, cols >= 0, row_stride >= cols")
+    if rows and cols:
+        span = (rows - 1) * row_stride + cols
+        avail = t.untyped_storage().nbytes() // t.element_size() - t.storage_offset()
+        if span > avail:
+            raise ValueError(f"region of {rows} x {cols} at stride {row_stride} ({span} elements) exceeds the "
+                             f"tensor's storage ({avail} elements from its start)")
 
 
 def _flat_arg(t: torch.Tensor):
@@ -234,6 +264,8 @@ def reduce_async(op: str, t: torch.Tensor, init=None, out: torch.Tensor | None =
     ptr, n, dt = _flat_arg(t)
     if out is None:
         out = torch.empty(1, dtype=t.dtype, device=t.device)
+    else:
+        _check_out(out, t, 1)
     ws = workspace(stream) if ws is None else ws
     box = _scalar(dt, init)
     _check(lib.ipm_reduce_async(op_code(op), dt, ptr, n, None if box is None else box.ctypes.data, out.data_ptr(),
@@ -257,8 +289,11 @@ def reduce_segmented(op: str, t: torch.Tensor, rows: int | None = None, cols: in
     elif rows is None or cols is None:
         raise ValueError("rows and cols are required for a flat tensor")
     row_stride = cols if row_stride is None else row_stride
+    _check_region(t, rows, cols, row_stride)
     if out is None:
         out = torch.empty(rows, dtype=t.dtype, device=t.device)
+    else:
+        _check_out(out, t, rows)
     ws = workspace(stream) if ws is None else ws
     box = _scalar(dt, init)
     _check(lib.ipm_reduce_segmented(op_code(op), dt, t.data_ptr(), rows, cols, row_stride,
@@ -277,6 +312,8 @@ def reduce_ragged(op: str, values: torch.Tensor, offsets: torch.Tensor, init=Non
     rows = offsets.numel() - 1
     if out is None:
         out = torch.empty(max(rows, 0), dtype=values.dtype, device=values.device)
+    else:
+        _check_out(out, values, rows)
     ws = workspace(stream) if ws is None else ws
     box = _scalar(dt, init)
     _check(lib.ipm_reduce_ragged(op_code(op), dt, ptr, offsets.data_ptr(), rows,
@@ -326,6 +363,7 @@ def reduce_2d(op: str, t: torch.Tensor, rows: int | None = None, cols: int | Non
     elif rows is None or cols is None:
         raise ValueError("rows and cols are required for a flat tensor")
     row_stride = cols if row_stride is None else row_stride
+    _check_region(t, rows, cols, row_stride)
     s = _stream(stream)
     ws = workspace(s) if ws is None else ws
     box = _scalar(dt, identity_value(op, dt) if init is None else init)
@@ -345,12 +383,16 @@ def reduce_fused_async(sig: str, x: torch.Tensor, y: torch.Tensor | None = None,
     ptr, n, dt = _flat_arg(x)
     yp = 0
     if f == FUSED["dot"]:
-        if y is None or y.numel() != n or y.dtype != x.dtype:
-            raise ValueError("dot needs y with the same length and dtype")
+        if y is None or y.numel() != n or y.dtype != x.dtype or y.device != x.device:
+            raise ValueError("dot needs y with the same length, dtype and device")
         yp = _flat_arg(y)[0]
     nv = lib.ipm_fused_nvars(f)
     if out is None:
         out = torch.empty(nv, dtype=x.dtype, device=x.device)
+    else:
+        _check_out(out, x, nv)
+    if init is not None and np.size(init) != nv:
+        raise ValueError(f"{sig} carries {nv} variables: init needs {nv} values")
     ws = workspace(stream) if ws is None else ws
     box = None if init is None else np.ascontiguousarray(init, dtype=NP_OF[dt])
     _check(lib.ipm_reduce_fused_async(f, dt, ptr, yp or None, n, None if box is None else box.ctypes.data,
@@ -367,8 +409,15 @@ def reduce_fused(sig: str, x: torch.Tensor, y: torch.Tensor | None = None, init=
         return out.cpu().numpy()
     f = FUSED[sig]
     ptr, n, dt = _flat_arg(x)
-    yp = _flat_arg(y)[0] if f == FUSED["dot"] else None
-    box = np.array(init, dtype=NP_OF[dt]).copy()
+    yp = None
+    if f == FUSED["dot"]:
+        if y is None or y.numel() != n or y.dtype != x.dtype or y.device != x.device:
+            raise ValueError("dot needs y with the same length, dtype and device")
+        yp = _flat_arg(y)[0]
+    nv = lib.ipm_fused_nvars(f)
+    box = np.array(init, dtype=NP_OF[dt]).reshape(-1).copy()
+    if box.size != nv:
+        raise ValueError(f"{sig} carries {nv} variables: init needs {nv} values")
     ws = workspace(stream) if ws is None else ws
     _check(lib.ipm_reduce_fused(f, dt, ptr, yp, n, box.ctypes.data, ws.data_ptr(), _stream(stream)),
            "ipm_reduce_fused")
@@ -397,17 +446,13 @@ def reduce_host(op: str, a, init=None, ws: torch.Tensor | None = None, stream=No
     return box[0]
 
 
+@functools.lru_cache(maxsize=None)
 def identity_value(op: str, dt: int):
-    """The identity of op on element type dt (SURVEY.md §8(c) identity column: 0, 1, the type's minimum /
-    maximum (-inf / +inf for floats), all ones, 0, 0, 1, 0). tests/test_gpu_parity.py checks that it equals what
-    the library's own finalize kernel returns for n = 0."""
-    op_code(op)  # unknown operator -> ValueError
-    np_t = np.dtype(NP_OF[dt])
-    if np_t.kind == "f":
-        lo, hi = -np.inf, np.inf
-    else:
-        lo, hi = np.iinfo(np_t).min, np.iinfo(np_t).max
-    return np_t.type({"+": 0, "*": 1, "max": lo, "min": hi, "&": -1, "|": 0, "^": 0, "&&": 1, "||": 0}[op])
+    """The identity of op on element type dt, from the library (ipm_identity): the value the synchronous calls
+    start from when the variable has no original value."""
+    box = np.zeros(1, dtype=NP_OF[dt])
+    _check(lib.ipm_identity(op_code(op), dt, box.ctypes.data), "ipm_identity")
+    return box[0]
 
 
 OPTIONS = {"flat_ctas_per_sm": 0, "seg_kernel": 1, "deterministic": 2, "dist_mode": 3, "dist_timeout_ms": 4}
@@ -429,6 +474,17 @@ def flat_geometry(dtype, n: int):
     g, b = ctypes.c_int(), ctypes.c_int()
     _check(lib.ipm_flat_geometry(dtype_code(dtype), n, ctypes.byref(g), ctypes.byref(b)), "ipm_flat_geometry")
     return g.value, b.value
+
+
+SCHEDULES = {-1: "none", 0: "static", 1: "guided", 2: "dynamic"}
+
+
+def flat_schedule(dtype, n: int) -> str:
+    """Which flat kernel the library launches for n elements under the current options (ipm_flat_schedule):
+    'static' (k_flat grid-stride), 'guided' (k_flat_guided), 'dynamic' (k_flat with a tile counter), 'none'."""
+    s = ctypes.c_int()
+    _check(lib.ipm_flat_schedule(dtype_code(dtype), n, ctypes.byref(s)), "ipm_flat_schedule")
+    return SCHEDULES[s.value]
 
 
 class KernelTimer:
@@ -575,11 +631,11 @@ class Comm:
                                                           "could not map every peer")
         return c
 
-    def __init__(self, rank: int, world: int, device: int, store=None, key: str = "ipm_nccl_id"):
+    @staticmethod
+    def bootstrap_id(rank: int, store, key: str = "ipm_nccl_id") -> bytes:
+        """Rank 0 makes the NCCL unique id (ipm_comm_unique_id) and publishes it in `store`; every rank returns the
+        same ipm_comm_id_bytes() bytes (host-only: no GPU is touched, so CPU tests drive it with gloo)."""
         nb = lib.ipm_comm_id_bytes()
-        if store is None:
-            import torch.distributed as dist
-            store = dist.distributed_c10d._get_default_store()
         if rank == 0:
             buf = ctypes.create_string_buffer(nb)
             _check(lib.ipm_comm_unique_id(buf), "ipm_comm_unique_id")
@@ -587,7 +643,14 @@ class Comm:
         uid = store.get(key)
         if len(uid) != nb:
             raise IpmError(10, "Comm", "bad NCCL id from store")
-        self._id = ctypes.create_string_buffer(uid, nb)
+        return uid
+
+    def __init__(self, rank: int, world: int, device: int, store=None, key: str = "ipm_nccl_id"):
+        if store is None:
+            import torch.distributed as dist
+            store = dist.distributed_c10d._get_default_store()
+        uid = self.bootstrap_id(rank, store, key)
+        self._id = ctypes.create_string_buffer(uid, len(uid))
         self._h = ctypes.c_void_p()
         torch.cuda.set_device(device)
         with _StdoutToStderr():
@@ -644,6 +707,8 @@ class Comm:
         ptr, n, dt = _flat_arg(shard)
         if out is None:
             out = torch.empty(1, dtype=shard.dtype, device=shard.device)
+        else:
+            _check_out(out, shard, 1)
         ws = workspace(stream) if ws is None else ws
         box = _scalar(dt, init)
         _check(lib.ipm_reduce_dist_async(self._h, op_code(op), dt, ptr, n, None if box is None else box.ctypes.data,

@@ -106,8 +106,14 @@ def test_c5_properties_and_prefix(ipm):
         got = ipm.reduce("+", x[lo:lo + cnt])
         _, want = oracle.reduce("+", x[lo:lo + cnt].cpu().numpy())
         assert got == np.float32(want)
-    # the whole 2^34: the sum of the per-(2^30) chunk reductions computed by the library in fp64 must agree
+    # the whole 2^34 against the oracle: the plain compensated left fold of the same generated input, streamed on
+    # the host cores in contiguous pieces merged in piece order (oracle.reduce_spec_split)
     full = ipm.reduce("+", x)
+    want_t, want_ld, _ = oracle.reduce_spec_split("+", spec, pieces=256)
+    assert abs(np.longdouble(full) - want_ld) <= TOL["float32"] * want_ld
+    # fp64 partial sums rounded once to float32: within one float32 ulp of the exact sum (far inside 1e-5)
+    assert abs(np.longdouble(full) - want_ld) <= np.longdouble(np.spacing(np.float32(want_t)))
+    # and the sum of the per-(2^30) chunk reductions computed by the library in fp64 agrees
     chunks = [ipm.reduce_async("+", x[i:i + (1 << 30)]).double() for i in range(0, n, 1 << 30)]
     total = float(torch.cat(chunks).sum())
     assert abs(float(full) - total) <= 1e-6 * total

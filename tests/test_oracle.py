@@ -447,3 +447,92 @@ def test_streaming_fold_equals_whole_fold():
     whole = oracle.reduce("+", ipmgen.fill_host(s))
     streamed = oracle.reduce_spec("+", s, chunk=65_536)
     assert whole[1] == streamed[1] and whole[0] == streamed[0]
+
+
+# --------------------------------------------------------------------------- split fold (ora_merge), the C5 oracle
+
+@pytest.mark.parametrize("dt", INT)
+def test_split_merge_closed_forms_int(dt):
+    # Σ_{i=1}^{n} i mod 2^w (closed form) through 7 pieces on 3 threads, and the generalised Wilson theorem
+    # (∏ of all odd residues mod 2^k is 1 for k >= 3) through pieces folded separately and merged
+    n = 3_000_001
+    s = ipmgen.Spec(dt, n, "iota", param=1)
+    v, ld, _ = oracle.reduce_spec_split("+", s, pieces=7, threads=3, chunk=100_000)
+    assert u(v, dt) == (n * (n + 1) // 2) % (1 << W[dt])
+    odd = np.arange(1, 1 << 20, 2, dtype=np.int64)          # all odd residues mod 2^20
+    f = oracle.Fold("*", "int64")
+    for part in np.array_split(odd, 9):
+        f.merge(oracle.Fold("*", "int64").fold(part))
+    assert int(f.result()[0]) % (1 << 20) == 1
+
+
+@pytest.mark.parametrize("op", list(oracle.OPS))
+@pytest.mark.parametrize("dt", INT)
+def test_split_merge_equals_bigint_fold(op, dt):
+    # any split of the iteration space, merged in order, gives the bits of a Python big-integer left fold
+    xs = ipmgen.fill_host(ipmgen.Spec(dt, 5000, "odd" if op == "*" else "random", seed=8))
+    if op in ("&&", "||"):
+        xs = xs % 3
+    mask = (1 << W[dt]) - 1
+    sg = lambda x: x - (1 << W[dt]) if x >> (W[dt] - 1) else x
+    r = 77
+    for x in xs.tolist():
+        x &= mask
+        r = {"+": lambda: (r + x) & mask, "*": lambda: (r * x) & mask, "max": lambda: r if sg(r) >= sg(x) else x,
+             "min": lambda: r if sg(r) <= sg(x) else x, "&": lambda: r & x, "|": lambda: r | x, "^": lambda: r ^ x,
+             "&&": lambda: int(r != 0 and x != 0), "||": lambda: int(r != 0 or x != 0)}[op]()
+    for cuts in ([2500], [1, 2, 3, 4999], [0, 0, 5000], list(range(0, 5000, 333))):
+        bounds = [0] + cuts + [5000]
+        f = oracle.Fold(op, dt, NPT[dt](77))
+        f.fold(xs[bounds[0]:bounds[1]])
+        for a, b in zip(bounds[1:-1], bounds[2:]):
+            f.merge(oracle.Fold(op, dt).fold(xs[a:b]))
+        assert u(f.result()[0], dt) == r, (op, cuts)
+
+
+@pytest.mark.parametrize("dt", FLT)
+def test_split_merge_float_sum(dt):
+    # i mod 1024 over n elements: closed form (n/1024)·523776, exact; random dyadic data: within 2^-60 of the
+    # exact sum (integers in units of the grid), as the unsplit compensated fold
+    n = 1 << 22
+    v, ld, _ = oracle.reduce_spec_split("+", ipmgen.Spec(dt, n, "mod", param=1024), pieces=13, threads=4)
+    assert ld == (n // 1024) * 523776 and v == (n // 1024) * 523776
+    s = ipmgen.Spec(dt, 1 << 20, "random", seed=4)
+    a = ipmgen.fill_host(s)
+    g = 14 if dt == "float32" else 43                       # the generator's dyadic grid, 2^-g (ipmgen.h)
+    exact = Fraction(sum((a.astype(np.float64) * 2.0**g).astype(np.int64).tolist()), 2**g)   # exact integers
+    _, ld, _ = oracle.reduce_spec_split("+", s, init=NPT[dt](0.25), pieces=64, threads=8, chunk=10_000)
+    assert abs(fr(ld) - (exact + Fraction(1, 4))) <= exact * Fraction(1, 2**60)
+    # compensation survives the merge: [1e20, 1] | [-1e20] must give 1 (a plain merge of s would give 0)
+    f = oracle.Fold("+", "float64").fold(np.array([1e20, 1.0]))
+    f.merge(oracle.Fold("+", "float64").fold(np.array([-1e20])))
+    assert f.result()[1] == 1
+
+
+@pytest.mark.parametrize("dt", FLT)
+def test_split_merge_float_product_and_extremes(dt):
+    # ±1 background with 64 planted factors: the exact product (Fraction) within the rounding bound
+    s = ipmgen.Spec(dt, 1 << 20, "signs", seed=3, plant="factor", nplant=64)
+    a = ipmgen.fill_host(s)
+    exact = Fraction(1)
+    for x in a.tolist():
+        if x != 1.0:
+            exact *= Fraction(x)
+    _, ld, _ = oracle.reduce_spec_split("*", s, pieces=10, threads=4)
+    assert abs(fr(ld) - exact) <= abs(exact) * Fraction(64, 2**63)
+    # IEEE maximum across pieces: -0 in one piece, +0 in a later one -> +0; NaN in any piece -> NaN
+    x = np.full(100, -1.0, NPT[dt]); x[10] = -0.0; x[90] = 0.0
+    f = oracle.Fold("max", dt).fold(x[:50]).merge(oracle.Fold("max", dt).fold(x[50:]))
+    assert struct.pack("<d", float(f.result()[0])) == struct.pack("<d", 0.0)
+    f = oracle.Fold("min", dt).fold(-x[:50]).merge(oracle.Fold("min", dt).fold(-x[50:]))
+    assert struct.pack("<d", float(f.result()[0])) == struct.pack("<d", -0.0)
+    x[60] = np.nan
+    f = oracle.Fold("max", dt).fold(x[:50]).merge(oracle.Fold("max", dt).fold(x[50:]))
+    assert np.isnan(f.result()[0])
+    # && / || across pieces: C truthiness of the pieces' values
+    y = np.ones(100, NPT[dt]); y[70] = -0.0
+    f = oracle.Fold("&&", dt).fold(y[:50]).merge(oracle.Fold("&&", dt).fold(y[50:]))
+    assert f.result()[0] == 0
+    z = np.zeros(100, NPT[dt]); z[99] = np.nan
+    f = oracle.Fold("||", dt).fold(z[:50]).merge(oracle.Fold("||", dt).fold(z[50:]))
+    assert f.result()[0] == 1

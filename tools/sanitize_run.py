@@ -80,3 +80,18 @@ for dt in TD:  # one CTA per row (long rows, many of them)
     ipm.reduce_segmented("+", x[1:], rows=600, cols=1100, row_stride=1100)
 torch.cuda.synchronize()
 print("sanitize_run (seg cta): ok")
+# the production flat schedule above 64 MiB: k_flat_guided (static tiles, dynamic chunks, remainder chunk), and
+# the dynamic / static k_flat selected by IPM_OPT_DETERMINISTIC, on misaligned inputs
+for dt, n in (("int32", 20_000_005), ("float32", 17_000_003), ("int64", 9_000_007), ("float64", 8_500_001)):
+    buf = torch.empty(n + 4, dtype=TD[dt], device="cuda")
+    x = buf[3:3 + n]
+    ipmgen.fill_device(ipmgen.Spec(dt, n, "random", seed=9), x.data_ptr(), 0, n, torch.cuda.current_stream().cuda_stream)
+    for det in (1, 0, 2):
+        ipm.set_option("deterministic", det)
+        assert ipm.flat_schedule(x.dtype, n) == {1: "guided", 0: "dynamic", 2: "static"}[det]
+        for op in ["+", "max"] + (["^"] if dt.startswith("int") else ["&&"]):
+            ipm.reduce(op, x, init=np.array(1, dtype=x.cpu()[:1].numpy().dtype)[()])
+    ipm.set_option("deterministic", 1)
+    del buf, x
+torch.cuda.synchronize()
+print("sanitize_run (guided > 64 MiB): ok")
