@@ -375,6 +375,16 @@ def suite(ipm, torch, ipmgen, peak):
             best = [d["read_probe_best_GBs"] for d in rows if "read_probe_best_GBs" in d]
             out["read_probe"] = {"best_GBs": best[0] if best else None,
                                  "variants": [d for d in rows if "probe" in d]}
+            # the same probe over 1 GiB (the C2 / C3 size): the per-call cost of a 1 GiB stream, the fair
+            # denominator for those rows
+            r = subprocess.run([probe, "1024"], capture_output=True, text=True, timeout=300)
+            rows = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+            best = [d["read_probe_best_GBs"] for d in rows if "read_probe_best_GBs" in d]
+            out["read_probe"]["best_GBs_1GiB"] = best[0] if best else None
+            if best:
+                for k, v in out.items():
+                    if isinstance(v, dict) and "GB/s" in v and (k.startswith("C2_float32") or k.startswith("C3_")):
+                        v["frac_of_read_probe_1GiB"] = v["GB/s"] / best[0]
         except (subprocess.TimeoutExpired, ValueError) as e:
             out["read_probe"] = {"error": str(e)[:200]}
     return out

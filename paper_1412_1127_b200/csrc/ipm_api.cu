@@ -60,6 +60,7 @@ static std::atomic<int> g_opt_seg_kernel{0}; // 0 auto (= 1), 1 warp per row (di
 static std::atomic<int> g_opt_deterministic{1};  // 1: guided deterministic schedule for the flat kernel
 static std::atomic<int> g_opt_dist_mode{0};      // 0: fused peer-memory exchange when mapped, 1: NCCL AllGather
 static std::atomic<long long> g_opt_dist_timeout_ms{30000};
+static std::atomic<int> g_opt_ragged_kernel{0};  // 0 auto (= 2), 1 one warp per element range, 2 CTA tiles
 static int flat_ctas_per_sm() {
   const int c = g_opt_flat_cps.load(std::memory_order_relaxed);
   if (c > 0) return c;
@@ -213,6 +214,24 @@ struct Launch {
     }();
     k_seg_warp<R, SEG_WARPS, SEG_U><<<seg_grid(p.rows, sms, occ), SEG_WARPS * 32, 0, st>>>(p);
   }
+  // CTA-tile ragged kernel (default): 128 threads x 4 vectors per thread per tile (32 float32 / 16 float64
+  // elements per thread), L2 bulk prefetch 2 tiles ahead, 4 CTAs per SM
+  static constexpr int RT_BLOCK = 128, RT_VPT = 4, RT_MINB = 4, RT_PFD = 2;
+  static cudaError_t ragged_tile(const RaggedParams& p, int blocks, cudaStream_t st) {
+    constexpr int smem = RaggedTile<R, RT_BLOCK, RT_VPT>::SMEM;
+    auto kern = k_ragged_tile<R, RT_BLOCK, RT_VPT, RT_MINB, RT_PFD>;
+    static const cudaError_t attr = [&] {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 (int)cudaSharedmemCarveoutMaxShared);
+      return e;
+    }();
+    if (attr != cudaSuccess) return attr;
+    kern<<<blocks, RT_BLOCK, smem, st>>>(p);
+    k_ragged_fix<R><<<(unsigned)((blocks + 7) / 8), 256, 0, st>>>(p, blocks);
+    return cudaSuccess;
+  }
   static void ragged(const RaggedParams& p, int blocks, int64_t nw, cudaStream_t st) {
     // 25 KiB of static shared memory per CTA: ask for the largest carveout so 8 CTAs fit on an SM
     // L2 prefetch of the next chunk (profiles/r01_sweep_ragged_5_l2prefetch.txt: +13-16 % on long rows, +1-7 % on
@@ -261,6 +280,7 @@ struct Table {
   void (*flat)(const FlatParams&, dim3, cudaStream_t);
   void (*two_d)(const Params2D&, int, int, cudaStream_t);  // (params, grid bound by the items, SM count, stream)
   void (*ragged)(const RaggedParams&, int, int64_t, cudaStream_t);
+  cudaError_t (*ragged_tile)(const RaggedParams&, int, cudaStream_t);
   void (*seg_warp)(const SegParams&, int, cudaStream_t);  // (params, SM count, stream)
   cudaError_t (*seg_tma)(const SegParams&, int, cudaStream_t);
   void (*seg_group)(const SegParams&, int, int, cudaStream_t);
@@ -271,7 +291,7 @@ struct Table {
 static const Table* table(ipm_op op, ipm_dtype dt) {
 #define IPM_ENTRY(O, D)                                                                                  \
   if (op == O && dt == D) {                                                                            \
-    static const Table t = {&Launch<O, D>::flat, &Launch<O, D>::two_d, &Launch<O, D>::ragged, &Launch<O, D>::seg_warp, &Launch<O, D>::seg_tma,     \
+    static const Table t = {&Launch<O, D>::flat, &Launch<O, D>::two_d, &Launch<O, D>::ragged, &Launch<O, D>::ragged_tile, &Launch<O, D>::seg_warp, &Launch<O, D>::seg_tma,     \
                             &Launch<O, D>::seg_group, &Launch<O, D>::finalize, &Launch<O, D>::exchange};\
     return &t;                                                                                         \
   }
@@ -561,6 +581,10 @@ ipm_status ipm_set_option(ipm_option key, int64_t value) {
     case IPM_OPT_DIST_TIMEOUT_MS:
       if (value < 1) break;
       g_opt_dist_timeout_ms = value;
+      return IPM_OK;
+    case IPM_OPT_RAGGED_KERNEL:
+      if (value < 0 || value > 2) break;
+      g_opt_ragged_kernel = (int)value;
       return IPM_OK;
   }
   set_error("unknown option or value out of range");
@@ -852,7 +876,9 @@ ipm_status ipm_reduce_ragged(ipm_op op, ipm_dtype dt, const void* dev, const int
   p.init = scalar_bits(dt, init);
   p.has_init = init != nullptr;
   p.out = dev_out;
-  const int64_t nw = std::min<int64_t>((int64_t)sm_count() * 32, WS_MAX_RAGGED_WARPS);  // 8 CTAs x 4 warps per SM
+  const int kern = g_opt_ragged_kernel.load(std::memory_order_relaxed);
+  const int64_t nw = kern == 1 ? std::min<int64_t>((int64_t)sm_count() * 32, WS_MAX_RAGGED_WARPS)  // 8 CTAs x 4 warps per SM
+                               : std::min<int64_t>((int64_t)sm_count() * 4, WS_MAX_RAGGED_WARPS);  // 4 CTAs per SM
   int64_t* base = (int64_t*)((char*)ws + WS_RAGGED);
   p.head_row = base;
   p.head_part = (uint64_t*)(base + WS_MAX_RAGGED_WARPS);
@@ -861,7 +887,8 @@ ipm_status ipm_reduce_ragged(ipm_op op, ipm_dtype dt, const void* dev, const int
   cudaStream_t st = (cudaStream_t)stream;
   {
     ProfScope ps(st, 4);
-    table(op, dt)->ragged(p, (int)(nw / 4), nw, st);
+    if (kern == 1) table(op, dt)->ragged(p, (int)(nw / 4), nw, st);
+    else CK(table(op, dt)->ragged_tile(p, (int)nw, st));
   }
   CK(cudaGetLastError());
   return IPM_OK;

@@ -279,9 +279,11 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_flat(FlatParams p) {
   const int64_t tail0 = head + nv * VW;
   const VT* vp = (const VT*)(a + head);
 
-  A acc[VW];
+  using LC = Loc<R>;
+  using L = typename LC::L;
+  L acc[VW];
 #pragma unroll
-  for (int k = 0; k < VW; ++k) acc[k] = R::id();
+  for (int k = 0; k < VW; ++k) acc[k] = LC::id();
 
   // a3: the hot loop — whole tiles of BLOCK*U vectors, U independent 256-bit loads in flight per thread
   const int64_t ntiles = nv / TILE;
@@ -293,7 +295,7 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_flat(FlatParams p) {
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
-      for (int k = 0; k < VW; ++k) acc[k] = R::op(acc[k], R::lift(v[u].w[k]));
+      LC::vec(acc, v[u]);
   };
   if (SCHED == 0) {
     #pragma unroll 1
@@ -318,7 +320,7 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_flat(FlatParams p) {
 #pragma unroll
       for (int u = 0; u < U; ++u)
 #pragma unroll
-        for (int k = 0; k < VW; ++k) acc[k] = R::op(acc[k], R::lift(cu[u].w[k]));
+        LC::vec(acc, cu[u]);
     }
   } else if (SCHED == 1) {
     const int64_t t1 = (ntiles * (blockIdx.x + 1)) / gridDim.x;
@@ -340,21 +342,21 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_flat(FlatParams p) {
        i += (int64_t)gridDim.x * BLOCK) {
     const VT v = ldv<HINT>(vp + i);
 #pragma unroll
-    for (int k = 0; k < VW; ++k) acc[k] = R::op(acc[k], R::lift(v.w[k]));
+    LC::vec(acc, v);
   }
   // head and tail scalars (< VW each)
   const int64_t g = (int64_t)blockIdx.x * BLOCK + threadIdx.x;
-  if (g < head) acc[0] = R::op(acc[0], R::lift(lds(a + g)));
-  if (g < n - tail0) acc[VW - 1] = R::op(acc[VW - 1], R::lift(lds(a + tail0 + g)));
+  if (g < head) acc[0] = LC::step(acc[0], lds(a + g));
+  if (g < n - tail0) acc[VW - 1] = LC::step(acc[VW - 1], lds(a + tail0 + g));
 
   // fold the private copies in a fixed tree
 #pragma unroll
   for (int s = VW / 2; s > 0; s >>= 1)
 #pragma unroll
-    for (int k = 0; k < s; ++k) acc[k] = R::op(acc[k], acc[k + s]);
+    for (int k = 0; k < s; ++k) acc[k] = LC::comb(acc[k], acc[k + s]);
 
   // a4 + a5
-  A cta = block_reduce<R, BLOCK>(acc[0], sm);
+  A cta = block_reduce<R, BLOCK>(LC::out(acc[0]), sm);
   grid_finish<R, BLOCK>(p, row, cta, sm);
 }
 
@@ -398,10 +400,12 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_flat_guided(FlatParams 
   const int64_t K = (rem + ct - 1) / ct;                 // dynamic chunks 0..K-1; chunk K = the remainder
   uint64_t* slots = p.partials;
 
-  A acc[VW];
+  using LC = Loc<R>;
+  using L = typename LC::L;
+  L acc[VW];
   auto reset = [&]() {
 #pragma unroll
-    for (int k = 0; k < VW; ++k) acc[k] = R::id();
+    for (int k = 0; k < VW; ++k) acc[k] = LC::id();
   };
   auto tile = [&](int64_t t) {
 #ifdef IPM_GUIDED_DEBUG
@@ -419,14 +423,14 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_flat_guided(FlatParams 
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
-      for (int k = 0; k < VW; ++k) acc[k] = R::op(acc[k], R::lift(v[u].w[k]));
+      LC::vec(acc, v[u]);
   };
   auto publish = [&](int64_t slot) {  // fixed tree: VW lanes -> warp -> CTA; one slot per element range
 #pragma unroll
     for (int s2 = VW / 2; s2 > 0; s2 >>= 1)
 #pragma unroll
-      for (int k = 0; k < s2; ++k) acc[k] = R::op(acc[k], acc[k + s2]);
-    const A t = block_reduce<R, BLOCK>(acc[0], sm);
+      for (int k = 0; k < s2; ++k) acc[k] = LC::comb(acc[k], acc[k + s2]);
+    const A t = block_reduce<R, BLOCK>(LC::out(acc[0]), sm);
     if (threadIdx.x == 0) __stcg(slots + slot, pack(t));
     __syncthreads();  // sm reuse
   };
@@ -452,7 +456,7 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_flat_guided(FlatParams 
 #pragma unroll
       for (int u = 0; u < U; ++u)
 #pragma unroll
-        for (int kk = 0; kk < VW; ++kk) acc[kk] = R::op(acc[kk], R::lift(cu[u].w[kk]));
+        LC::vec(acc, cu[u]);
     }
   };
   reset();
@@ -478,10 +482,10 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_flat_guided(FlatParams 
       for (int64_t i = ntiles * TILE + threadIdx.x; i < nv; i += BLOCK) {
         const VT v = ldv(vp + i);
 #pragma unroll
-        for (int k = 0; k < VW; ++k) acc[k] = R::op(acc[k], R::lift(v.w[k]));
+        LC::vec(acc, v);
       }
-      if (threadIdx.x < head) acc[0] = R::op(acc[0], R::lift(lds(a + threadIdx.x)));
-      if (threadIdx.x < n - tail0) acc[VW - 1] = R::op(acc[VW - 1], R::lift(lds(a + tail0 + threadIdx.x)));
+      if (threadIdx.x < head) acc[0] = LC::step(acc[0], lds(a + threadIdx.x));
+      if (threadIdx.x < n - tail0) acc[VW - 1] = LC::step(acc[VW - 1], lds(a + tail0 + threadIdx.x));
     }
     publish(G + c);
     c = s_c;
@@ -555,9 +559,11 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_2d(Params2D q) {
   // item it = (row r, chunk c), it = r * per_row + c, stepped by nw without a division per item
   const int64_t dr = nw / per_row, dc = nw - dr * per_row;
   int64_t r = gw / per_row, c = gw - r * per_row;
-  A acc[VW];
+  using LC = Loc<R>;
+  using L = typename LC::L;
+  L acc[VW];
 #pragma unroll
-  for (int k = 0; k < VW; ++k) acc[k] = R::id();
+  for (int k = 0; k < VW; ++k) acc[k] = LC::id();
   for (int64_t it = gw; it < items; it += nw) {
     if (PF && lane == 0 && it + nw < items) {  // the warp's next item (row, chunk) into L2
       int64_t rn = r + dr, cn = c + dc;
@@ -582,17 +588,17 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_2d(Params2D q) {
 #pragma unroll
       for (int u = 0; u < U; ++u)
 #pragma unroll
-        for (int k = 0; k < VW; ++k) acc[k] = R::op(acc[k], R::lift(v[u].w[k]));
+        LC::vec(acc, v[u]);
     } else {
       for (int64_t i = v0; i < nv; i += 32) {
         const VT v = ldv(vp + i);
 #pragma unroll
-        for (int k = 0; k < VW; ++k) acc[k] = R::op(acc[k], R::lift(v.w[k]));
+        LC::vec(acc, v);
       }
     }
     if (c == 0) {
-      if (lane < head) acc[0] = R::op(acc[0], R::lift(lds(a + lane)));
-      if (lane < q.cols - tail0) acc[VW - 1] = R::op(acc[VW - 1], R::lift(lds(a + tail0 + lane)));
+      if (lane < head) acc[0] = LC::step(acc[0], lds(a + lane));
+      if (lane < q.cols - tail0) acc[VW - 1] = LC::step(acc[VW - 1], lds(a + tail0 + lane));
     }
     r += dr;
     c += dc;
@@ -604,8 +610,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_2d(Params2D q) {
 #pragma unroll
   for (int s = VW / 2; s > 0; s >>= 1)
 #pragma unroll
-    for (int k = 0; k < s; ++k) acc[k] = R::op(acc[k], acc[k + s]);
-  A cta = block_reduce<R, BLOCK>(acc[0], sm);
+    for (int k = 0; k < s; ++k) acc[k] = LC::comb(acc[k], acc[k + s]);
+  A cta = block_reduce<R, BLOCK>(LC::out(acc[0]), sm);
   grid_finish<R, BLOCK>(q.f, 0, cta, sm);
 }
 
@@ -625,6 +631,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_seg_warp(SegParams p) {
   using A = typename R::A;
   using VT = typename Vec<B>::T;
   constexpr int VW = Vec<B>::W;
+  using LC = Loc<R>;
+  using L = typename LC::L;
   const int lane = threadIdx.x & 31;
   const int64_t gw = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5);
   const int64_t nw = (int64_t)gridDim.x * WARPS;
@@ -639,9 +647,9 @@ __global__ void __launch_bounds__(WARPS * 32) k_seg_warp(SegParams p) {
     const int64_t nv = (n - head) / VW;
     const int64_t tail0 = head + nv * VW;
     const VT* vp = (const VT*)(a + head);
-    A acc[VW];
+    L acc[VW];
 #pragma unroll
-    for (int k = 0; k < VW; ++k) acc[k] = R::id();
+    for (int k = 0; k < VW; ++k) acc[k] = LC::id();
     int64_t i = lane;
     #pragma unroll 1
     for (; i + (U - 1) * 32 < nv; i += U * 32) {
@@ -651,20 +659,20 @@ __global__ void __launch_bounds__(WARPS * 32) k_seg_warp(SegParams p) {
 #pragma unroll
       for (int u = 0; u < U; ++u)
 #pragma unroll
-        for (int k = 0; k < VW; ++k) acc[k] = R::op(acc[k], R::lift(v[u].w[k]));
+        LC::vec(acc, v[u]);
     }
     for (; i < nv; i += 32) {
       const VT v = ldv<HINT>(vp + i);
 #pragma unroll
-      for (int k = 0; k < VW; ++k) acc[k] = R::op(acc[k], R::lift(v.w[k]));
+      LC::vec(acc, v);
     }
-    if (lane < head) acc[0] = R::op(acc[0], R::lift(lds(a + lane)));
-    if (lane < n - tail0) acc[VW - 1] = R::op(acc[VW - 1], R::lift(lds(a + tail0 + lane)));
+    if (lane < head) acc[0] = LC::step(acc[0], lds(a + lane));
+    if (lane < n - tail0) acc[VW - 1] = LC::step(acc[VW - 1], lds(a + tail0 + lane));
 #pragma unroll
     for (int s = VW / 2; s > 0; s >>= 1)
 #pragma unroll
-      for (int k = 0; k < s; ++k) acc[k] = R::op(acc[k], acc[k + s]);
-    A t = R::warp(acc[0]);
+      for (int k = 0; k < s; ++k) acc[k] = LC::comb(acc[k], acc[k + s]);
+    A t = R::warp(LC::out(acc[0]));
     if (lane == 0) {
       if (p.has_init) t = R::op(R::lift((B)p.init), t);
       ((B*)p.out)[r] = R::fin(t);
@@ -1181,6 +1189,292 @@ __global__ void __launch_bounds__(256) k_ragged_fix(RaggedParams p, int64_t nw) 
   if (lane == 0) {
     if (p.has_init) acc = R::op(R::lift((B)p.init), acc);
     ((B*)p.out)[row] = R::fin(acc);
+  }
+}
+
+
+// ------------------------------------------------------------------------------------------ ragged, CTA tiles
+// The same clause and ownership rules as k_ragged_vec, with the CTA (not the warp) as the unit: CTA b owns the
+// element range [lo, hi) = [P0 + b*nnz/G, P0 + (b+1)*nnz/G) and every row whose first element lies in it, and
+// streams it in tiles of BLOCK x EPT elements (EPT contiguous elements per thread, VPT 32-byte loads issued at the
+// start of the tile; thread 0 asks L2 for the tile PFD tiles ahead with one bulk prefetch, so the loads hit L2 and
+// HBM bytes stay in flight without holding registers). Per tile:
+//   1. row setup, one thread per row: the rows that start in the tile are the next rows in order (rows are
+//      sorted by their start), so thread i takes row rs + i (one coalesced 8-byte offset load, the window
+//      prefetched during the previous tile), flags the row's first element in the owning thread's 32-bit flag
+//      word (atomicOr) and records the row id at that position; an empty row is finished on the spot. A window
+//      of BLOCK rows that is entirely inside the tile repeats the step with the next BLOCK rows.
+//   2. a tile in which no row starts (inside a long row) is folded into per-thread running values, no scan; they
+//      are reduced into the open row's value once, when the next row start (or the range end) comes.
+//   3. otherwise the lane fold: each thread folds its EPT elements once; at a flagged element the running value
+//      (the segment that ends there) is parked in the thread's shared-memory column and the accumulator restarts;
+//      rows that start and end inside the thread are finished from the parked values.
+//   4. a segmented scan over the CTA's threads (warp shuffles, then one thread chains the NW warp totals with
+//      the open row carried in from the previous tile) gives each flagged thread the value of the row that ends
+//      at its first flag.
+// Rows continued from the previous CTA or into the next one leave head / tail records, finished by
+// k_ragged_fix (one record pair per CTA instead of per warp).
+template <class R, int BLOCK, int VPT>
+struct RaggedTile {
+  static constexpr int EPT = Vec<typename R::B>::W * VPT;
+  static constexpr int SMEM = EPT * BLOCK * ((int)sizeof(typename R::A) + 4);
+};
+template <class R, int BLOCK, int VPT, int MINB, int PFD>
+__global__ void __launch_bounds__(BLOCK, MINB) k_ragged_tile(RaggedParams p) {
+  using B = typename R::B;
+  using A = typename R::A;
+  using VT = typename Vec<B>::T;
+  constexpr int VW = Vec<B>::W;
+  constexpr int EPT = VW * VPT;     // elements per thread per tile (one flag bit each)
+  constexpr int TILE = BLOCK * EPT;
+  constexpr int NW = BLOCK / 32;
+  static_assert(EPT <= 32, "one 32-bit flag word per thread");
+  __shared__ unsigned s_flag[BLOCK];      // bit k of word t: a row starts at the thread's element k
+  // dynamic shared memory (RaggedTile<>::SMEM bytes):
+  //   s_val [k][t]: value of the segment that ends just before a flagged element (column per thread)
+  //   s_rid [k][t]: the row starting there (valid where flagged)
+  extern __shared__ __align__(16) unsigned char ragged_dsm[];
+  A* s_val = (A*)ragged_dsm;
+  int* s_rid = (int*)(ragged_dsm + (size_t)EPT * BLOCK * sizeof(A));
+  __shared__ A s_wv[NW], s_pv[NW], s_red[NW];
+  __shared__ long long s_wr[NW], s_pr[NW];
+  __shared__ int s_wf[NW];
+  __shared__ int s_any[2];                // per tile parity: some row starts in the tile
+  __shared__ A s_cv;                      // the row open at the end of the last tile, and its id
+  __shared__ long long s_cr;
+  __shared__ long long s_rs;
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const unsigned lanemask_lt = (1u << lane) - 1u;
+  const int64_t b = blockIdx.x, G = gridDim.x;
+  const B* a = (const B*)p.a;
+  const int64_t rows = p.rows;
+  const int64_t P0 = __ldg(p.off), P1 = __ldg(p.off + rows);
+  const int64_t nnz = P1 - P0;
+  const int64_t lo = P0 + (int64_t)(((__int128)nnz * b) / G);
+  const int64_t hi = P0 + (int64_t)(((__int128)nnz * (b + 1)) / G);
+  if (wid == 0) {
+    const int64_t r0 = warp_lower_bound(p.off, rows, lo);  // first row starting at or after lo
+    if (lane == 0) s_rs = r0;
+  }
+  if (t == 0) s_any[0] = s_any[1] = 0;
+  __syncthreads();
+  int64_t rs = s_rs;
+  const int64_t hrow = (rs > 0 && lo < hi && __ldg(p.off + rs) > lo) ? rs - 1 : -1;  // spans lo from before
+  if (t == 0) {
+    p.head_row[b] = lo < hi ? -1 : -2;
+    p.tail_row[b] = -1;
+    s_cv = R::id();
+    s_cr = hrow;
+  }
+  auto finish = [&](int64_t row, A v) {
+    if (p.has_init) v = R::op(R::lift((B)p.init), v);
+    ((B*)p.out)[row] = R::fin(v);
+  };
+  // tiles start at 32-byte aligned element positions at or below lo
+  const int64_t q0 = lo - (int64_t)(((uintptr_t)(a + lo) & 31u) / sizeof(B));
+  auto prefetch_tile = [&](int64_t Bc) {  // one thread: the tile's bytes into L2
+    if (Bc < hi) {
+      const int64_t e0 = Bc > lo ? Bc : lo;
+      const int64_t e1 = Bc + TILE < hi ? Bc + TILE : hi;
+      l2_prefetch(a + e0, (e1 - e0) * (int64_t)sizeof(B));
+    }
+  };
+  // the first window of row offsets of the next tile: thread i holds off[rs + i] (and lane 31 off[rs + i + 1])
+  int64_t wo = 0, wo31 = 0;
+  auto fetch_window = [&](int64_t base) {
+    const int64_t r = base + t;
+    wo = r <= rows ? __ldg(p.off + r) : INT64_MAX;
+    wo31 = (lane == 31 && r + 1 <= rows) ? __ldg(p.off + r + 1) : INT64_MAX;
+  };
+  if (lo < hi) {
+    fetch_window(rs);
+    if (t == 0)
+      for (int d = 1; d < PFD; ++d) prefetch_tile(q0 + (int64_t)d * TILE);
+  }
+  A run = R::id();          // flag-free tiles: this thread's elements of the open row, not yet in s_cv
+  bool pending = false;     // CTA-uniform: some thread's `run` holds elements
+  auto flush_runs = [&]() {  // s_cv ⊕= the runs (thread order); ends with a barrier
+    const A tot = block_reduce<R, BLOCK>(run, s_red);
+    if (t == 0) s_cv = R::op(s_cv, tot);
+    run = R::id();
+    pending = false;
+    __syncthreads();
+  };
+  int par = 0;
+#pragma unroll 1
+  for (int64_t Bc = q0; Bc < hi; Bc += TILE, par ^= 1) {
+    const int rlo = (int)(lo > Bc ? lo - Bc : 0);
+    const int rhi = (int)(hi - Bc < TILE ? hi - Bc : TILE);
+    const bool interior = rlo == 0 && rhi == TILE;  // CTA-uniform
+    const int64_t tile_end = Bc + rhi;
+    if (t == 0) prefetch_tile(Bc + (int64_t)PFD * TILE);
+    // this tile's elements: loads issued now, consumed after the row setup
+    B x[EPT];
+    {
+      const B* pl = a + Bc + (int64_t)t * EPT;
+      if (interior) {
+#pragma unroll
+        for (int v = 0; v < VPT; ++v) {
+          const VT w = ldv((const VT*)(pl + v * VW));
+#pragma unroll
+          for (int k = 0; k < VW; ++k) x[v * VW + k] = w.w[k];
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < EPT; ++k) {
+          const int rel = t * EPT + k;
+          x[k] = (rel >= rlo && rel < rhi) ? lds(pl + k) : (B)0;
+        }
+      }
+    }
+    s_flag[t] = 0u;
+    if (t == 0) s_any[par ^ 1] = 0;  // the next tile's word (this tile's was cleared two tiles ago)
+    __syncthreads();  // flags cleared; the previous tile's readers of s_rid / s_val are done
+    // 1. row setup
+#pragma unroll 1
+    while (true) {
+      const int64_t r = rs + t;
+      const int64_t o = wo;
+      const int64_t up = __shfl_down_sync(FULL, o, 1);
+      const int64_t e = lane == 31 ? wo31 : up;  // off[r + 1]
+      const bool in = r < rows && o < tile_end;
+      const bool starts = in && e > o;
+      if (starts) {
+        const int pos = (int)(o - Bc);
+        const int tt = pos / EPT, k = pos - tt * EPT;
+        atomicOr(&s_flag[tt], 1u << k);
+        s_rid[k * BLOCK + tt] = (int)r;
+      } else if (in) {
+        finish(r, R::id());  // an empty row
+      }
+      if (__ballot_sync(FULL, starts) && lane == 0) s_any[par] = 1;
+      const int cnt = __syncthreads_count(in);  // also publishes the flags
+      rs += cnt;
+      if (cnt < BLOCK) break;
+      fetch_window(rs);  // every row of the window starts in this tile: the next BLOCK rows
+    }
+    fetch_window(rs);  // the next tile's first window, in flight while this tile is folded
+    if (!s_any[par]) {
+      // 2. no row starts here: every element continues the open row
+      if (interior) {
+#pragma unroll
+        for (int k = 0; k < EPT; ++k) run = R::op(run, R::lift(x[k]));
+      } else {
+#pragma unroll
+        for (int k = 0; k < EPT; ++k) {
+          const int rel = t * EPT + k;
+          run = R::op(run, (rel >= rlo && rel < rhi) ? R::lift(x[k]) : R::id());
+        }
+      }
+      pending = true;
+      continue;
+    }
+    if (pending) flush_runs();
+    // 3. lane fold, parking the value of every segment that ends at a flagged element
+    const unsigned fl = s_flag[t];
+    A acc = R::id();
+    if (interior) {
+#pragma unroll
+      for (int k = 0; k < EPT; ++k) {
+        const bool sf = (fl >> k) & 1u;
+        if (sf) s_val[k * BLOCK + t] = acc;
+        acc = R::op(sf ? R::id() : acc, R::lift(x[k]));
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < EPT; ++k) {
+        const int rel = t * EPT + k;
+        const bool sf = (fl >> k) & 1u;
+        if (sf) s_val[k * BLOCK + t] = acc;
+        acc = R::op(sf ? R::id() : acc, (rel >= rlo && rel < rhi) ? R::lift(x[k]) : R::id());
+      }
+    }
+    const int kf = fl ? __ffs(fl) - 1 : 0;
+    const int kl = fl ? 31 - __clz(fl) : 0;
+    const A head = fl ? s_val[kf * BLOCK + t] : acc;  // elements before the first flag
+    const A cur = fl ? acc : R::id();                 // from the last flag on
+    for (unsigned m = fl & ~(1u << kl); m; m &= m - 1) {  // rows that start and end inside this thread
+      const int k0 = __ffs(m) - 1;
+      const int k1 = __ffs(fl & ~((2u << k0) - 1u)) - 1;
+      finish(s_rid[k0 * BLOCK + t], s_val[k1 * BLOCK + t]);
+    }
+    const long long my_rid = fl ? (long long)s_rid[kl * BLOCK + t] : -1;
+    // 4. segmented scan over the threads: a flagged thread starts a segment with `cur`
+    const bool F = fl != 0u;
+    const unsigned bal = __ballot_sync(FULL, F);
+    const unsigned le = bal & (lanemask_lt | (1u << lane));
+    const int start = le ? 31 - __clz(le) : 0;
+    A sv = F ? cur : head;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const A ov = shfl_up_acc(sv, d);
+      if (lane - d >= start) sv = R::op(ov, sv);
+    }
+    const long long wlast_rid = __shfl_sync(FULL, my_rid, bal ? 31 - __clz(bal) : 0);
+    if (lane == 31) {
+      s_wv[wid] = sv;
+      s_wf[wid] = bal != 0u;
+      s_wr[wid] = wlast_rid;
+    }
+    __syncthreads();
+    if (t == 0) {  // the row open at each warp's start, in warp order, and at the tile's end
+      A P = s_cv;
+      long long PR = s_cr;
+#pragma unroll
+      for (int w2 = 0; w2 < NW; ++w2) {
+        s_pv[w2] = P;
+        s_pr[w2] = PR;
+        if (s_wf[w2]) {
+          P = s_wv[w2];
+          PR = s_wr[w2];
+        } else {
+          P = R::op(P, s_wv[w2]);
+        }
+      }
+      s_cv = P;
+      s_cr = PR;
+    }
+    __syncthreads();
+    const A P = s_pv[wid];
+    const long long PR = s_pr[wid];
+    const unsigned lt = bal & lanemask_lt;
+    const A ev = shfl_up_acc(sv, 1);
+    const long long rr = __shfl_sync(FULL, my_rid, lt ? 31 - __clz(lt) : 0);
+    const A E = lt ? ev : (lane == 0 ? P : R::op(P, ev));  // the row open at this thread's start
+    const long long ER = lt ? rr : PR;
+    if (F && ER >= 0) {  // ... ends at this thread's first flag
+      const A v = R::op(E, head);
+      if (ER == hrow) {
+        p.head_row[b] = hrow;
+        p.head_part[b] = pack(v);
+      } else {
+        finish(ER, v);
+      }
+    }
+  }
+  if (pending) flush_runs();
+  __syncthreads();
+  // the row still open at hi
+  if (t == 0 && lo < hi) {
+    const long long orid = s_cr;
+    const A ov = s_cv;
+    if (orid >= 0) {
+      if (orid == hrow) {
+        p.head_row[b] = hrow;
+        p.head_part[b] = pack(ov);
+      } else if (__ldg(p.off + orid + 1) <= hi) {
+        finish(orid, ov);
+      } else {
+        p.tail_row[b] = orid;
+        p.tail_part[b] = pack(ov);
+      }
+    }
+  }
+  // the last CTA also owns the empty rows that start at P1 (after every element)
+  if (b == G - 1 && wid == 0) {
+    const int64_t r = warp_lower_bound(p.off, rows, P1);
+    for (int64_t q = r + lane; q < rows; q += 32)
+      if (__ldg(p.off + q) == __ldg(p.off + q + 1)) finish(q, R::id());
   }
 }
 

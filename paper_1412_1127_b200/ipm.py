@@ -92,6 +92,8 @@ def _load():
         "ipm_reduce_dist_async": ([vp, ci, ci, vp, i64, vp, vp, vp, vp], ci),
     }
     for name, (args, res) in sigs.items():
+        if "IPM_LIB" in os.environ and not hasattr(L, name):
+            continue  # an older build loaded for a same-box A/B (tools/ab_lib.py): calls it lacks fail when used
         f = getattr(L, name)  # AttributeError if the library does not export it: fail loudly
         f.argtypes = args
         f.restype = res
@@ -455,7 +457,9 @@ def identity_value(op: str, dt: int):
     return box[0]
 
 
-OPTIONS = {"flat_ctas_per_sm": 0, "seg_kernel": 1, "deterministic": 2, "dist_mode": 3, "dist_timeout_ms": 4}
+OPTIONS = {"flat_ctas_per_sm": 0, "seg_kernel": 1, "deterministic": 2, "dist_mode": 3, "dist_timeout_ms": 4,
+           "ragged_kernel": 5}
+RAGGED_KERNELS = {"auto": 0, "warp": 1, "tile": 2}
 DIST_MODES = {"auto": 0, "p2p": 0, "nccl": 1}
 SEG_KERNELS = {"auto": 0, "warp": 1, "ldg": 1, "tma": 2}
 
@@ -467,6 +471,8 @@ def set_option(key: str, value) -> None:
         value = SEG_KERNELS[value]
     if key == "dist_mode" and isinstance(value, str):
         value = DIST_MODES[value]
+    if key == "ragged_kernel" and isinstance(value, str):
+        value = RAGGED_KERNELS[value]
     _check(lib.ipm_set_option(OPTIONS[key], int(value)), "ipm_set_option")
 
 

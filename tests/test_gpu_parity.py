@@ -410,10 +410,25 @@ def ragged_cases():
     d[100:400] = np.arange(300) % 5
     d[-3:] = 0
     yield "long_rows", ipmgen.offsets_from_degrees(d, 1)
+    # thousands of empty rows inside one tile (the per-tile row window repeats), rows of one element, a row
+    # spanning many CTAs, rows ending exactly where others start
+    d = np.ones(200_000, np.int64)
+    d[5000:15000] = 0
+    d[50_000] = 3_000_000
+    d[60_000:60_100] = 4096
+    d[-5000:] = 0
+    yield "empties_and_giant", ipmgen.offsets_from_degrees(d, 7)
+
+
+@pytest.fixture(params=["tile", "warp"])
+def ragged_kernel(request, ipm):
+    ipm.set_option("ragged_kernel", request.param)
+    yield request.param
+    ipm.set_option("ragged_kernel", "auto")
 
 
 @pytest.mark.parametrize("op,dt", LEGAL)
-def test_ragged_parity(ipm, op, dt):
+def test_ragged_parity(ipm, op, dt, ragged_kernel):
     for k, (name, off) in enumerate(ragged_cases()):
         n = int(off[-1]) + 5
         spec = workload(op, dt, n, seed=k + 21)
@@ -429,7 +444,7 @@ def test_ragged_parity(ipm, op, dt):
             assert got.tobytes() == want_t.tobytes(), (op, dt, name)
 
 
-def test_ragged_big_powerlaw_deterministic(ipm):
+def test_ragged_big_powerlaw_deterministic(ipm, ragged_kernel):
     off = ipmgen.offsets_from_degrees(ipmgen.degrees(1 << 20, seed=7))
     spec = ipmgen.Spec("float32", int(off[-1]), "random", seed=7)
     x = device_input(spec)

@@ -214,3 +214,32 @@ def test_fused_multi_round_parity(ipm, sig, dt):
         got = ipm.reduce_fused(sig, x, y if sig == "dot" else None, init=init)
         for v, op in enumerate(ops):
             check(op, dt, got[v], want_t[v], want_ld[v])
+
+
+@pytest.mark.parametrize("dt", ["float32", "float64"])
+def test_float_edges_segmented_and_2d(ipm, dt):
+    """IEEE maximum / minimum and C truthiness (R10, R5) through the row kernels and the 2-D kernel: rows of
+    negatives with a -0 / +0 / NaN planted at varying lanes and positions, against the oracle row by row."""
+    rows, cols, stride = 300, 1000, 1003
+    base = -np.abs(ipmgen.fill_host(ipmgen.Spec(dt, rows * stride, "signed", seed=8))) - NPT[dt](1)
+    rng = np.random.default_rng(3)
+    for op in ("max", "min", "&&", "||"):
+        a = base.copy() if op != "min" else -base
+        if op == "||":
+            a = np.zeros_like(base)
+            a[::3] = NPT[dt](-0.0)
+        r_idx = rng.integers(0, rows, 60)
+        c_idx = rng.integers(0, cols, 60)
+        for j, (r, c) in enumerate(zip(r_idx, c_idx)):
+            v = [NPT[dt](-0.0), NPT[dt](0.0), NPT[dt](np.nan)][j % 3]
+            a[r * stride + c] = v
+        x = _upload(a, 1)
+        for kern in ("warp", "tma"):
+            ipm.set_option("seg_kernel", kern)
+            got = ipm.reduce_segmented(op, x, rows=rows, cols=cols, row_stride=stride).cpu().numpy()
+            want, _ = oracle.reduce_segmented(op, a, rows, cols, stride)
+            assert got.tobytes() == want.tobytes(), (op, kern)
+        ipm.set_option("seg_kernel", "auto")
+        got = ipm.reduce_2d(op, x, rows=rows, cols=cols, row_stride=stride)
+        want = oracle.reduce(op, _region(a, rows, cols, stride))[0]
+        assert bits(got, dt) == bits(want, dt), op

@@ -1,12 +1,13 @@
 // read_probe.cu — read-only HBM roofline probe ("measure a read-only roofline probe"): the
 // simplest streaming read that can saturate HBM, independent of the product kernels. Each thread XOR-folds
 // 256-bit vectors (ld.global.nc.L1::no_allocate.L2::evict_first, U independent loads in flight) over a grid-stride
-// loop of an 8 GiB buffer (far above L2) and writes one word. Variants over U and resident CTAs; CUDA events,
+// loop of an 8 GiB buffer (far above L2; or the size given in MiB) and writes one word. Variants over U and resident CTAs; CUDA events,
 // median of 20 launches. Prints one JSON object per variant and a final {"read_probe_best_GBs": ...}.
 #include <cuda_runtime.h>
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { fprintf(stderr, "CUDA %s at %d\n", cudaGetErrorString(e), __LINE__); exit(1);} } while (0)
@@ -59,10 +60,11 @@ double run(const V8* a, int64_t nv, uint32_t* sink, int sms) {
   return gbs;
 }
 
-int main() {
+int main(int argc, char** argv) {
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
-  const int64_t bytes = (int64_t)8 << 30;
+  // optional argument: buffer size in MiB (default 8192; the bench also runs 1024 = the C2 / C3 size)
+  const int64_t bytes = (int64_t)(argc > 1 ? atoll(argv[1]) : 8192) << 20;
   V8* a; uint32_t* sink;
   CK(cudaMalloc(&a, bytes));
   CK(cudaMemset(a, 0x5a, bytes));

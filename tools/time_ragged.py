@@ -7,7 +7,8 @@ from paper_1412_1127_b200 import ipm
 
 CASES = [("powerlaw", 1 << 24, 16.0), ("const", 1 << 22, 64.0), ("uniform", 1 << 24, 16.0),
          ("const", 1 << 16, 4096.0), ("const", 1 << 25, 4.0)]
-OPS = [("+", "float32"), ("max", "float32"), ("+", "float64"), ("^", "int32")]
+OPS = [("+", "float32"), ("max", "float32"), ("+", "float64"), ("^", "int32"), ("max", "float64")]
+KERNELS = ["warp", "tile"]
 if len(sys.argv) > 1 and sys.argv[1] == "quick":
     OPS = OPS[:1]
 for kind, rows, mean in CASES:
@@ -23,13 +24,18 @@ for kind, rows, mean in CASES:
         while time.perf_counter() - t0 < 0.2:
             ipm.reduce_ragged(op, vals, offs, out=o)
             torch.cuda.synchronize()
-        with ipm.KernelTimer(20) as kt:
-            for _ in range(20):
-                ipm.reduce_ragged(op, vals, offs, out=o)
+        for kern in KERNELS:
+            ipm.set_option("ragged_kernel", kern)
+            ipm.reduce_ragged(op, vals, offs, out=o)
             torch.cuda.synchronize()
-        med = statistics.median(kt.ms)
-        w = vals.element_size()
-        nbytes = nnz * w + off.size * 8 + rows * w
-        print(f"{kind:8s} rows={rows:9d} mean={mean:6.0f} {op:3s} {dt:7s} nnz={nnz} max={int(np.diff(off).max())}: "
-              f"{med:.3f} ms {nbytes/med/1e6:7.1f} GB/s", flush=True)
+            with ipm.KernelTimer(20) as kt:
+                for _ in range(20):
+                    ipm.reduce_ragged(op, vals, offs, out=o)
+                torch.cuda.synchronize()
+            med = statistics.median(kt.ms)
+            w = vals.element_size()
+            nbytes = nnz * w + off.size * 8 + rows * w
+            print(f"{kern:5s} {kind:8s} rows={rows:9d} mean={mean:6.0f} {op:3s} {dt:7s} nnz={nnz} "
+                  f"max={int(np.diff(off).max())}: {med:.3f} ms {nbytes/med/1e6:7.1f} GB/s", flush=True)
+        ipm.set_option("ragged_kernel", "auto")
         del vals, o
