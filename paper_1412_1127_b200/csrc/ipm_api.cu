@@ -60,7 +60,7 @@ static std::atomic<int> g_opt_seg_kernel{0}; // 0 auto (= 1), 1 warp per row (di
 static std::atomic<int> g_opt_deterministic{1};  // 1: guided deterministic schedule for the flat kernel
 static std::atomic<int> g_opt_dist_mode{0};      // 0: fused peer-memory exchange when mapped, 1: NCCL AllGather
 static std::atomic<long long> g_opt_dist_timeout_ms{30000};
-static std::atomic<int> g_opt_ragged_kernel{0};  // 0 auto (= 2), 1 one warp per element range, 2 CTA tiles
+static std::atomic<int> g_opt_ragged_kernel{0};  // 0 auto (= 1), 1 one warp per element range, 2 CTA tiles
 static int flat_ctas_per_sm() {
   const int c = g_opt_flat_cps.load(std::memory_order_relaxed);
   if (c > 0) return c;
@@ -876,7 +876,8 @@ ipm_status ipm_reduce_ragged(ipm_op op, ipm_dtype dt, const void* dev, const int
   p.init = scalar_bits(dt, init);
   p.has_init = init != nullptr;
   p.out = dev_out;
-  const int kern = g_opt_ragged_kernel.load(std::memory_order_relaxed);
+  const int kopt = g_opt_ragged_kernel.load(std::memory_order_relaxed);
+  const int kern = kopt == 0 ? 1 : kopt;  // auto = the warp kernel (measured faster, profiles/r02_time_ragged_*)
   const int64_t nw = kern == 1 ? std::min<int64_t>((int64_t)sm_count() * 32, WS_MAX_RAGGED_WARPS)  // 8 CTAs x 4 warps per SM
                                : std::min<int64_t>((int64_t)sm_count() * 4, WS_MAX_RAGGED_WARPS);  // 4 CTAs per SM
   int64_t* base = (int64_t*)((char*)ws + WS_RAGGED);
