@@ -1236,12 +1236,12 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_ragged_tile(RaggedParams p) {
   extern __shared__ __align__(16) unsigned char ragged_dsm[];
   A* s_val = (A*)ragged_dsm;
   int* s_rid = (int*)(ragged_dsm + (size_t)EPT * BLOCK * sizeof(A));
-  __shared__ A s_wv[NW], s_pv[NW], s_red[NW];
-  __shared__ long long s_wr[NW], s_pr[NW];
+  __shared__ A s_wv[NW], s_red[NW];
+  __shared__ long long s_wr[NW];
   __shared__ int s_wf[NW];
   __shared__ int s_any[2];                // per tile parity: some row starts in the tile
-  __shared__ A s_cv;                      // the row open at the end of the last tile, and its id
-  __shared__ long long s_cr;
+  __shared__ A s_cv[2];                   // the row open at the end of the last flagged tile, and its id (by the
+  __shared__ long long s_cr[2];           // parity q of flagged tiles: read in one, written for the next)
   __shared__ long long s_rs;
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const unsigned lanemask_lt = (1u << lane) - 1u;
@@ -1256,6 +1256,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_ragged_tile(RaggedParams p) {
     const int64_t r0 = warp_lower_bound(p.off, rows, lo);  // first row starting at or after lo
     if (lane == 0) s_rs = r0;
   }
+  s_flag[t] = 0u;
   if (t == 0) s_any[0] = s_any[1] = 0;
   __syncthreads();
   int64_t rs = s_rs;
@@ -1263,8 +1264,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_ragged_tile(RaggedParams p) {
   if (t == 0) {
     p.head_row[b] = lo < hi ? -1 : -2;
     p.tail_row[b] = -1;
-    s_cv = R::id();
-    s_cr = hrow;
+    s_cv[0] = R::id();
+    s_cr[0] = hrow;
   }
   auto finish = [&](int64_t row, A v) {
     if (p.has_init) v = R::op(R::lift((B)p.init), v);
@@ -1293,9 +1294,10 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_ragged_tile(RaggedParams p) {
   }
   A run = R::id();          // flag-free tiles: this thread's elements of the open row, not yet in s_cv
   bool pending = false;     // CTA-uniform: some thread's `run` holds elements
+  int q = 0;                // CTA-uniform: parity of the flagged tiles so far
   auto flush_runs = [&]() {  // s_cv ⊕= the runs (thread order); ends with a barrier
     const A tot = block_reduce<R, BLOCK>(run, s_red);
-    if (t == 0) s_cv = R::op(s_cv, tot);
+    if (t == 0) s_cv[q] = R::op(s_cv[q], tot);
     run = R::id();
     pending = false;
     __syncthreads();
@@ -1327,9 +1329,9 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_ragged_tile(RaggedParams p) {
         }
       }
     }
-    s_flag[t] = 0u;
+    // (no barrier here: every thread cleared its own flag word when it read it, and the previous tile's readers of
+    // s_rid / s_val / s_any finished before its last barrier)
     if (t == 0) s_any[par ^ 1] = 0;  // the next tile's word (this tile's was cleared two tiles ago)
-    __syncthreads();  // flags cleared; the previous tile's readers of s_rid / s_val are done
     // 1. row setup
 #pragma unroll 1
     while (true) {
@@ -1372,6 +1374,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_ragged_tile(RaggedParams p) {
     if (pending) flush_runs();
     // 3. lane fold, parking the value of every segment that ends at a flagged element
     const unsigned fl = s_flag[t];
+    s_flag[t] = 0u;  // ready for the next tile's setup (which runs after this tile's scan barrier)
     A acc = R::id();
     if (interior) {
 #pragma unroll
@@ -1417,26 +1420,17 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_ragged_tile(RaggedParams p) {
       s_wr[wid] = wlast_rid;
     }
     __syncthreads();
-    if (t == 0) {  // the row open at each warp's start, in warp order, and at the tile's end
-      A P = s_cv;
-      long long PR = s_cr;
-#pragma unroll
-      for (int w2 = 0; w2 < NW; ++w2) {
-        s_pv[w2] = P;
-        s_pr[w2] = PR;
-        if (s_wf[w2]) {
-          P = s_wv[w2];
-          PR = s_wr[w2];
-        } else {
-          P = R::op(P, s_wv[w2]);
-        }
+    // the row open at this warp's start: the tile's carry-in folded with the earlier warps, in warp order
+    A P = s_cv[q];
+    long long PR = s_cr[q];
+    for (int w2 = 0; w2 < wid; ++w2) {
+      if (s_wf[w2]) {
+        P = s_wv[w2];
+        PR = s_wr[w2];
+      } else {
+        P = R::op(P, s_wv[w2]);
       }
-      s_cv = P;
-      s_cr = PR;
     }
-    __syncthreads();
-    const A P = s_pv[wid];
-    const long long PR = s_pr[wid];
     const unsigned lt = bal & lanemask_lt;
     const A ev = shfl_up_acc(sv, 1);
     const long long rr = __shfl_sync(FULL, my_rid, lt ? 31 - __clz(lt) : 0);
@@ -1451,13 +1445,18 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_ragged_tile(RaggedParams p) {
         finish(ER, v);
       }
     }
+    if (t == BLOCK - 1) {  // the row open at the end of the tile, for the next flagged tile
+      s_cv[q ^ 1] = bal ? sv : R::op(P, sv);
+      s_cr[q ^ 1] = bal ? wlast_rid : PR;
+    }
+    q ^= 1;
   }
   if (pending) flush_runs();
   __syncthreads();
   // the row still open at hi
   if (t == 0 && lo < hi) {
-    const long long orid = s_cr;
-    const A ov = s_cv;
+    const long long orid = s_cr[q];
+    const A ov = s_cv[q];
     if (orid >= 0) {
       if (orid == hrow) {
         p.head_row[b] = hrow;

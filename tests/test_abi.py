@@ -113,3 +113,41 @@ def test_shard_ranges(ipm):
 def test_workspace_layout(ipm):
     assert ipm.WS_BYTES >= 8192 + 8 * 4096
     assert ipm.lib.ipm_comm_id_bytes() == 128
+
+
+def test_identity_matches_oracle(ipm):
+    """ipm_identity (the start value of the synchronous calls when the variable has none) equals the oracle's
+    empty fold for all 30 legal pairs, bit for bit; illegal pairs are refused."""
+    import numpy as np
+    import oracle
+    NP = {"int32": np.int32, "int64": np.int64, "float32": np.float32, "float64": np.float64}
+    U = {"int32": np.uint32, "int64": np.uint64, "float32": np.uint32, "float64": np.uint64}
+    n = 0
+    for op in ipm.OPS:
+        for dt in NP:
+            code = {"int32": 0, "int64": 1, "float32": 2, "float64": 3}[dt]
+            box = np.zeros(1, NP[dt])
+            rc = ipm.lib.ipm_identity(ipm.OPS[op], code, box.ctypes.data)
+            if not oracle.legal(op, dt):
+                assert rc == 1  # IPM_E_REDOP
+                continue
+            assert rc == 0
+            want = np.array([oracle.identity(op, dt)], NP[dt])
+            assert box.view(U[dt])[0] == want.view(U[dt])[0], (op, dt, box, want)
+            n += 1
+    assert n == 30
+    assert ipm.lib.ipm_identity(0, 0, None) == 3
+
+
+def test_flat_schedule_query(ipm):
+    import torch
+    assert ipm.flat_schedule(torch.float32, 0) == "none"
+    assert ipm.flat_schedule(torch.float32, 1 << 24) == "static"
+    assert ipm.flat_schedule(torch.float32, (1 << 24) + 1) == "guided"
+    ipm.set_option("deterministic", 0)
+    try:
+        assert ipm.flat_schedule(torch.int64, 1 << 30) == "dynamic"
+        ipm.set_option("deterministic", 2)
+        assert ipm.flat_schedule(torch.int64, 1 << 30) == "static"
+    finally:
+        ipm.set_option("deterministic", 1)

@@ -24,7 +24,9 @@ def main():
     ap.add_argument("--dtype", default="float32")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--log2n", type=int, default=None)
+    ap.add_argument("--seg-kernel", default="auto", choices=["auto", "warp", "tma"])
     a = ap.parse_args()
+    ipm.set_option("seg_kernel", a.seg_kernel)
     n = {"c1": 1 << 20, "c2": 1 << 28, "c3": 65536 * 4096, "c4": 1 << 30, "c5": 1 << 34, "stats": 1 << 28,
          "dot": 1 << 29, "2d": 16384 * 16384}[a.config]
     if a.log2n:

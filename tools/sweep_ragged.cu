@@ -62,6 +62,41 @@ void run(const char* name, const Data& d) {
          bytes / ms / 1e6, (long long)bad);
 }
 
+template <class R, int BLOCK, int VPT, int MINB, int PFD>
+void run_tile(const char* name, const Data& d) {
+  using B = typename R::B;
+  auto kern = k_ragged_tile<R, BLOCK, VPT, MINB, PFD>;
+  constexpr int smem = RaggedTile<R, BLOCK, VPT>::SMEM;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared));
+  int maxb = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&maxb, kern, BLOCK, smem));
+  const int blocks = d.sms * std::min(MINB, maxb);
+  RaggedParams p{};
+  p.a = d.a; p.off = d.off; p.rows = d.rows; p.init = 0; p.has_init = 0; p.out = d.out;
+  int64_t* base = (int64_t*)d.ws;
+  p.head_row = base; p.head_part = (uint64_t*)(base + 8192); p.tail_row = base + 2 * 8192;
+  p.tail_part = (uint64_t*)(base + 3 * 8192);
+  auto f = [&] {
+    kern<<<blocks, BLOCK, smem>>>(p);
+    k_ragged_fix<R><<<(unsigned)((blocks + 7) / 8), 256>>>(p, blocks);
+  };
+  float ms = time_ms(f, 20);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  std::vector<B> got(d.rows), ref(d.rows);
+  CK(cudaMemcpy(got.data(), d.out, d.rows * sizeof(B), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(ref.data(), d.ref, d.rows * sizeof(B), cudaMemcpyDeviceToHost));
+  int64_t bad = 0;
+  for (int64_t i = 0; i < d.rows; ++i) {
+    const double g = (double)got[i], r = (double)ref[i];
+    if (!(g == r || (g - r) * (g - r) <= 1e-20 * r * r + 1e-30)) ++bad;
+  }
+  const double bytes = d.nnz * sizeof(B) + (d.rows + 1) * 8.0 + d.rows * sizeof(B);
+  printf("%-4s tile BLOCK=%d VPT=%d MINB=%d PFD=%d occ=%d  %7.3f ms  %7.1f GB/s  mismatches=%lld\n", name, BLOCK, VPT, MINB,
+         PFD, maxb, ms, bytes / ms / 1e6, (long long)bad);
+}
+
 template <class R>
 void all(const char* name, Data d) {
   using B = typename R::B;
@@ -72,13 +107,17 @@ void all(const char* name, Data d) {
   {  // reference: the product configuration
     run<R, 4, 8, 2, false>(name, Data{d.a, d.off, d.rows, d.nnz, d.ref, d.ws, d.ref, d.sms});
   }
-  run<R, 4, 8, 2, true>(name, d);
-  run<R, 4, 8, 2, true, 1>(name, d);
-  run<R, 4, 8, 2, true, 2>(name, d);
-  run<R, 4, 8, 2, true, -1>(name, d);
-  run<R, 4, 8, 2, true, -2>(name, d);
-  run<R, 4, 8, 2, true, -3>(name, d);
-  run<R, 4, 8, 2, true>(name, d);
+  constexpr int PFV = sizeof(typename R::A) > sizeof(typename R::B) ? -1 : 1;  // the product's warp kernel
+  run<R, 4, 8, 2, true, PFV>(name, d);
+  run_tile<R, 128, 4, 4, 2>(name, d);
+  run_tile<R, 128, 4, 4, 3>(name, d);
+  run_tile<R, 128, 2, 6, 2>(name, d);
+  run_tile<R, 128, 2, 8, 2>(name, d);
+  run_tile<R, 256, 2, 3, 2>(name, d);
+  run_tile<R, 256, 2, 4, 2>(name, d);
+  run_tile<R, 64, 4, 8, 2>(name, d);
+  run_tile<R, 64, 2, 12, 2>(name, d);
+  run<R, 4, 8, 2, true, PFV>(name, d);
   CK(cudaFree(d.a)); CK(cudaFree(d.out)); CK(cudaFree(d.ref));
 }
 
