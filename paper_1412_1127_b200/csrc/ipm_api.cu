@@ -244,6 +244,36 @@ struct Launch {
     k_ragged_vec<R, 4, 8, 2, true, PFV><<<blocks, 128, 0, st>>>(p);  // 8 CTAs x 4 warps per SM, 2 vectors per lane
     k_ragged_fix<R><<<(unsigned)((nw + 7) / 8), 256, 0, st>>>(p, nw);
   }
+  // rank-order ragged kernel: RR_WARPS warps per CTA, 2 vectors per lane, offset ring of RR_NR windows; as many CTAs
+  // per SM as fit (shared memory bound), the grid one full wave of them
+#ifndef IPM_RR_WARPS
+#define IPM_RR_WARPS 4
+#endif
+#ifndef IPM_RR_MINB
+#define IPM_RR_MINB 6
+#endif
+#ifndef IPM_RR_NR
+#define IPM_RR_NR 8
+#endif
+#ifndef IPM_RR_K
+#define IPM_RR_K 8
+#endif
+  static constexpr int RR_WARPS = IPM_RR_WARPS, RR_MINB = IPM_RR_MINB, RR_VPL = 2, RR_NR = IPM_RR_NR, RR_K = IPM_RR_K;
+  static constexpr int RR_PFV = sizeof(typename R::A) > sizeof(typename R::B) ? -1 : 1;
+  static int ragged_rank_ctas_per_sm() {
+    static const int occ = [] {
+      auto kern = k_ragged_rank<R, RR_WARPS, RR_MINB, RR_VPL, RR_NR, RR_PFV>;
+      cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+      int m = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m, kern, RR_WARPS * 32, 0);
+      return m > 0 ? m : 1;
+    }();
+    return occ;
+  }
+  static void ragged_rank(const RaggedParams& p, int blocks, int64_t nw, cudaStream_t st) {
+    k_ragged_rank<R, RR_WARPS, RR_MINB, RR_VPL, RR_NR, RR_PFV><<<blocks, RR_WARPS * 32, 0, st>>>(p);
+    k_ragged_fix<R><<<(unsigned)((nw + 7) / 8), 256, 0, st>>>(p, nw);
+  }
   // 8-byte folds run 3 CTAs x 256 per SM with up to 85 registers (+1-3 % over 4 CTAs at 64 registers; 4-byte folds
   // lose up to 17 % that way, profiles/r01_ab_2d_minb.txt). max_grid = SMs x the resident CTAs per SM.
   static constexpr int TWO_D_MINB = sizeof(typename R::B) == 8 ? 3 : 4;
@@ -281,6 +311,8 @@ struct Table {
   void (*two_d)(const Params2D&, int, int, cudaStream_t);  // (params, grid bound by the items, SM count, stream)
   void (*ragged)(const RaggedParams&, int, int64_t, cudaStream_t);
   cudaError_t (*ragged_tile)(const RaggedParams&, int, cudaStream_t);
+  void (*ragged_rank)(const RaggedParams&, int, int64_t, cudaStream_t);
+  int (*ragged_rank_ctas_per_sm)();
   void (*seg_warp)(const SegParams&, int, cudaStream_t);  // (params, SM count, stream)
   cudaError_t (*seg_tma)(const SegParams&, int, cudaStream_t);
   void (*seg_group)(const SegParams&, int, int, cudaStream_t);
@@ -291,7 +323,7 @@ struct Table {
 static const Table* table(ipm_op op, ipm_dtype dt) {
 #define IPM_ENTRY(O, D)                                                                                  \
   if (op == O && dt == D) {                                                                            \
-    static const Table t = {&Launch<O, D>::flat, &Launch<O, D>::two_d, &Launch<O, D>::ragged, &Launch<O, D>::ragged_tile, &Launch<O, D>::seg_warp, &Launch<O, D>::seg_tma,     \
+    static const Table t = {&Launch<O, D>::flat, &Launch<O, D>::two_d, &Launch<O, D>::ragged, &Launch<O, D>::ragged_tile, &Launch<O, D>::ragged_rank, &Launch<O, D>::ragged_rank_ctas_per_sm, &Launch<O, D>::seg_warp, &Launch<O, D>::seg_tma,     \
                             &Launch<O, D>::seg_group, &Launch<O, D>::finalize, &Launch<O, D>::exchange};\
     return &t;                                                                                         \
   }
@@ -583,7 +615,7 @@ ipm_status ipm_set_option(ipm_option key, int64_t value) {
       g_opt_dist_timeout_ms = value;
       return IPM_OK;
     case IPM_OPT_RAGGED_KERNEL:
-      if (value < 0 || value > 2) break;
+      if (value < 0 || value > 3) break;
       g_opt_ragged_kernel = (int)value;
       return IPM_OK;
   }
@@ -878,8 +910,12 @@ ipm_status ipm_reduce_ragged(ipm_op op, ipm_dtype dt, const void* dev, const int
   p.out = dev_out;
   const int kopt = g_opt_ragged_kernel.load(std::memory_order_relaxed);
   const int kern = kopt == 0 ? 1 : kopt;  // auto = the warp kernel (measured faster, profiles/r02_time_ragged_*)
-  const int64_t nw = kern == 1 ? std::min<int64_t>((int64_t)sm_count() * 32, WS_MAX_RAGGED_WARPS)  // 8 CTAs x 4 warps per SM
-                               : std::min<int64_t>((int64_t)sm_count() * 4, WS_MAX_RAGGED_WARPS);  // 4 CTAs per SM
+  const Table* tb = table(op, dt);
+  const int64_t nw = kern == 1   ? std::min<int64_t>((int64_t)sm_count() * 32, WS_MAX_RAGGED_WARPS)  // 8 CTAs x 4 warps per SM
+                     : kern == 3 ? (int64_t)std::min<int64_t>((int64_t)sm_count() * tb->ragged_rank_ctas_per_sm(),
+                                                              WS_MAX_RAGGED_WARPS / IPM_RR_WARPS) *
+                                           IPM_RR_WARPS  // one wave of CTAs
+                                 : std::min<int64_t>((int64_t)sm_count() * 4, WS_MAX_RAGGED_WARPS);  // 4 CTAs per SM
   int64_t* base = (int64_t*)((char*)ws + WS_RAGGED);
   p.head_row = base;
   p.head_part = (uint64_t*)(base + WS_MAX_RAGGED_WARPS);
@@ -888,8 +924,9 @@ ipm_status ipm_reduce_ragged(ipm_op op, ipm_dtype dt, const void* dev, const int
   cudaStream_t st = (cudaStream_t)stream;
   {
     ProfScope ps(st, 4);
-    if (kern == 1) table(op, dt)->ragged(p, (int)(nw / 4), nw, st);
-    else CK(table(op, dt)->ragged_tile(p, (int)nw, st));
+    if (kern == 1) tb->ragged(p, (int)(nw / 4), nw, st);
+    else if (kern == 3) tb->ragged_rank(p, (int)(nw / IPM_RR_WARPS), nw, st);
+    else CK(tb->ragged_tile(p, (int)nw, st));
   }
   CK(cudaGetLastError());
   return IPM_OK;

@@ -1193,6 +1193,270 @@ __global__ void __launch_bounds__(256) k_ragged_fix(RaggedParams p, int64_t nw) 
 }
 
 
+// ------------------------------------------------------------------------------------------ ragged, row order
+// k_ragged_rank: the ownership rules, chunk shape and lane fold of k_ragged_vec, with the per-chunk row bookkeeping
+// rebuilt so that every row is examined once, by one lane, which later finishes it (round 2;
+// profiles/r01_ncu_ragged5_*: the window / flag-map loop of k_ragged_vec cost ~175 of ~474 warp instructions per
+// chunk, the per-lane finish loop ~65, and 30 % of the stall samples sat on the register copy that shifts the
+// offset window; profiles/r02_ncu_rrank_* record the variants measured on the way here):
+//  - row offsets come through a per-warp shared-memory ring of NR windows of 32 offsets (entry (r - r0) mod 32*NR
+//    holds off[r]), filled by cp.async up to NR-3 windows ahead of the first row not yet examined; no register
+//    holds an in-flight offset;
+//  - each chunk reads the 64 offsets from its first unexamined row on (two LDS per lane; a chunk in which more
+//    than 64 rows start reads further groups): lane i owns rows nxt+i and nxt+32+i, flags their starts (shared
+//    atomicOr) and keeps start and end relative to the chunk in registers (later groups re-read them);
+//  - the lane fold parks the value of every segment that ends at a flag in the lane's own shared-memory column
+//    (as k_ragged_vec); after the segmented warp scan the lane that holds a row's first piece adds the pieces
+//    before it; then each owning lane reads its row's value at the row's END position (where the next row
+//    starts) and stores out[row]: consecutive rows from consecutive lanes, no per-lane loop, no row map.
+//  Positions are kept relative to the chunk and rows relative to r0 in 32 bits.
+__device__ __forceinline__ void cp_async8(void* s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(s)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <class R, int WARPS, int MINB, int VPL, int NR, int PFV = 0>
+__global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_rank(RaggedParams p) {
+  using B = typename R::B;
+  using A = typename R::A;
+  using VT = typename Vec<B>::T;
+  constexpr int VW = Vec<B>::W;
+  constexpr int EPL = VW * VPL;  // elements per lane per chunk (one flag bit each)
+  constexpr int CH = 32 * EPL;   // elements per chunk
+  constexpr int RING = 32 * NR;  // offset ring entries
+  static_assert(EPL <= 32 && (EPL & (EPL - 1)) == 0, "flag word");
+  static_assert(NR >= 4 && (NR & (NR - 1)) == 0, "offset ring: a power of two >= 4 windows");
+  // per warp, column-major by lane (position EPL*l + k at [k*32 + l]: a lane's column is bank-conflict free)
+  __shared__ A s_val[WARPS][CH];             // value of the segment that ends just before a flagged position
+  __shared__ unsigned s_flag[WARPS][32];     // per lane: bit k = a row starts at the lane's element k
+  __shared__ int64_t s_off[WARPS][RING];     // offset ring
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  A* val = s_val[wid];
+  A* val_col = s_val[wid] + lane;
+  unsigned* flagw = s_flag[wid];
+  int64_t* ring = s_off[wid];
+  flagw[lane] = 0u;
+  const unsigned lanemask_lt = (1u << lane) - 1u;
+  const int64_t w = (int64_t)blockIdx.x * WARPS + wid;
+  const int64_t nw = (int64_t)gridDim.x * WARPS;
+  const B* a = (const B*)p.a;
+  const int64_t rows = p.rows;
+  const int64_t P0 = __ldg(p.off), P1 = __ldg(p.off + rows);
+  const int64_t nnz = P1 - P0;
+  const int64_t lo = P0 + (int64_t)(((__int128)nnz * w) / nw);
+  const int64_t hi = P0 + (int64_t)(((__int128)nnz * (w + 1)) / nw);
+  const int64_t r0 = warp_lower_bound(p.off, rows, lo);
+  const int64_t hrow = (r0 > 0 && lo < hi && __ldg(p.off + r0 - 1) < lo && __ldg(p.off + r0) > lo) ? r0 - 1 : -1;
+  const int nrel = (int)(rows - r0);  // rows from r0 on (rows < 2^31)
+  if (lane == 0) {
+    p.head_row[w] = lo < hi ? -1 : -2;
+    p.tail_row[w] = -1;
+  }
+  const bool has_init = p.has_init;
+  const A ia = has_init ? R::lift((B)p.init) : R::id();
+  B* const outw = (B*)p.out + r0;  // rows relative to r0
+  auto fin = [&](A v) { return R::fin(has_init ? R::op(ia, v) : v); };
+  auto col = [](unsigned d) { return (d % EPL) * 32 + d / EPL; };  // chunk position -> column address
+  // chunk bases are 32-byte aligned positions from q0; positions below are relative to the chunk
+  const int64_t q0 = lo - (int64_t)(((uintptr_t)(a + lo) & 31u) / sizeof(B));
+  const int hrel = (int)(hi - q0), lrel = (int)(lo - q0);  // warp range relative to q0 (< 2^31)
+  // offset ring: window k = rows r0 + 32k .. +31 (offsets clamped to off[rows] = P1) lands in ring[32 (k % NR) ..]
+  int nxt = 0;     // first row not yet examined, relative to r0
+  int issued = 0;  // windows issued so far
+  auto refill = [&]() {  // windows nxt/32 .. nxt/32 + 2 complete, up to NR - 3 more in flight
+    const int bw = nxt >> 5;
+    if (issued < bw + NR) {
+      if (issued < bw + NR - 3) cp_async_wait<0>();  // a jump: no copy may still target a slot reused below
+      for (int k = issued > bw ? issued : bw; k < bw + NR; ++k) {
+        const int64_t r = r0 + 32 * (int64_t)k + lane;
+        cp_async8(&ring[32 * (k & (NR - 1)) + lane], p.off + (r < rows ? r : rows));
+        cp_async_commit();
+      }
+      issued = bw + NR;
+    }
+    cp_async_wait<NR - 3>();
+    __syncwarp();
+  };
+  long long open_rid = hrow;  // the row open at the chunk start (-1: none)
+  A open_val = R::id();
+  constexpr int PFD = PFV < 0 ? -PFV : PFV;
+  bool pf_on = PFV > 0;
+  auto prefetch = [&](int pb) {  // pb relative to q0
+    if (PFV != 0 && lane == 0 && pf_on && pb < hrel) {
+      const uint32_t bytes = (uint32_t)((hrel - pb < CH ? hrel - pb : CH) * (int)sizeof(B)) & ~15u;
+      if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a + q0 + pb), "r"(bytes) : "memory");
+    }
+  };
+  if (lrel < hrel) {
+#pragma unroll 1
+    for (int d = 1; d < PFV; ++d) prefetch(d * CH);
+    const B* pl = a + q0 + EPL * lane;
+#pragma unroll 1
+    for (int cb = 0; cb < hrel; cb += CH, pl += CH) {
+      prefetch(cb + PFD * CH);
+      const int rlo_c = lrel > cb ? lrel - cb : 0;
+      const int rhi_c = hrel - cb < CH ? hrel - cb : CH;
+      const bool interior = rlo_c == 0 && rhi_c == CH;  // warp-uniform
+      B x[EPL];
+      if (interior) {
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+          const VT t = ldv((const VT*)(pl + v * VW));
+#pragma unroll
+          for (int k = 0; k < VW; ++k) x[v * VW + k] = t.w[k];
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < EPL; ++k) {
+          const int rel = EPL * lane + k;
+          x[k] = (rel >= rlo_c && rel < rhi_c) ? lds(pl + k) : (B)0;
+        }
+      }
+      // rows starting in the chunk's valid range (every unexamined row starts at or after the chunk and lo), in
+      // groups of 64 from row c0: lane i holds rows c0 + 64g + i and c0 + 64g + 32 + i (starts d, ends e)
+      const int64_t qc = q0 + cb;
+      auto rel = [&](int64_t o) { const int64_t d = o - qc; return d < (int64_t)INT32_MAX ? (int)d : INT32_MAX; };
+      const int c0 = nxt;
+      int dA = 0, eA = 0, dB = 0, eB = 0;  // group 0
+      int F = 0;                           // non-empty rows starting in the chunk
+      int first_d = 0, last_put = -1;      // start of the first of them, row of the last (relative to r0)
+#pragma unroll 1
+      for (int g = 0;; ++g) {
+        refill();
+        const int base = nxt & (RING - 1);
+        const int d1 = rel(ring[(base + lane) & (RING - 1)]);
+        const int d2 = rel(ring[(base + 32 + lane) & (RING - 1)]);
+        const int d3 = rel(ring[(base + 64) & (RING - 1)]);
+        const int u1 = __shfl_down_sync(FULL, d1, 1), u2 = __shfl_down_sync(FULL, d2, 1);
+        const int f2 = __shfl_sync(FULL, d2, 0);
+        const int e1 = lane == 31 ? f2 : u1, e2 = lane == 31 ? d3 : u2;
+        const bool in1 = nxt + lane < nrel && d1 < rhi_c;
+        const bool in2 = nxt + 32 + lane < nrel && d2 < rhi_c;
+        const bool p1 = in1 && e1 > d1, p2 = in2 && e2 > d2;
+        if (p1) atomicOr(&flagw[(unsigned)d1 / EPL], 1u << ((unsigned)d1 % EPL));
+        if (p2) atomicOr(&flagw[(unsigned)d2 / EPL], 1u << ((unsigned)d2 % EPL));
+        const unsigned m1 = __ballot_sync(FULL, p1), m2 = __ballot_sync(FULL, p2);
+        if (m1 | m2) {
+          if (F == 0) first_d = m1 ? __shfl_sync(FULL, d1, __ffs(m1) - 1) : __shfl_sync(FULL, d2, __ffs(m2) - 1);
+          last_put = m2 ? nxt + 63 - __clz(m2) : nxt + 31 - __clz(m1);
+        }
+        F += __popc(m1) + __popc(m2);
+        if (g == 0) {
+          dA = d1; eA = e1; dB = d2; eB = e2;
+        }
+        // the in-range rows are a prefix of the 64
+        const int nin = __popc(__ballot_sync(FULL, in1)) + __popc(__ballot_sync(FULL, in2));
+        nxt += nin;
+        if (nin < 64) break;
+      }
+      __syncwarp();
+      if (F == 0) {  // no row starts in the chunk (empty rows: finished below): every element continues open_rid
+        A v = R::id();
+        if (interior) {
+#pragma unroll
+          for (int k = 0; k < EPL; ++k) v = R::op(v, R::lift(x[k]));
+        } else {
+#pragma unroll
+          for (int k = 0; k < EPL; ++k) {
+            const int rel = EPL * lane + k;
+            v = R::op(v, (rel >= rlo_c && rel < rhi_c) ? R::lift(x[k]) : R::id());
+          }
+        }
+        open_val = R::op(open_val, R::warp(v));
+        if (PFV < 0) pf_on = true;
+      } else {
+        if (PFV < 0) pf_on = false;
+        const unsigned fl = flagw[lane];
+        flagw[lane] = 0u;
+        // lane-local segmented fold, one pass: at every flagged element the running value (the segment that
+        // ends there) is parked in the lane's own shared-memory column and the accumulator restarts
+        A acc = R::id();
+        if (interior) {
+#pragma unroll
+          for (int k = 0; k < EPL; ++k) {
+            const bool s = (fl >> k) & 1u;
+            if (s) val_col[k * 32] = acc;
+            acc = R::op(s ? R::id() : acc, R::lift(x[k]));
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < EPL; ++k) {
+            const int rel = EPL * lane + k;
+            const bool s = (fl >> k) & 1u;
+            if (s) val_col[k * 32] = acc;
+            acc = R::op(s ? R::id() : acc, (rel >= rlo_c && rel < rhi_c) ? R::lift(x[k]) : R::id());
+          }
+        }
+        // segmented inclusive scan over lanes: a flagged lane starts a segment with its tail value
+        const bool flag = fl != 0u;
+        const unsigned bal = __ballot_sync(FULL, flag);
+        const unsigned le = bal & (lanemask_lt | (1u << lane));
+        const int start = le ? 31 - __clz(le) : 0;
+        A sv = acc;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const A ov = shfl_up_acc(sv, d);
+          if (lane - d >= start) sv = R::op(ov, sv);
+        }
+        // the pieces before a flagged lane's first row start complete the row open at the lane's start
+        A ev = shfl_up_acc(sv, 1);
+        if (!(bal & lanemask_lt)) ev = lane == 0 ? open_val : R::op(open_val, ev);
+        if (flag) {
+          A* h = val_col + (__ffs(fl) - 1) * 32;
+          *h = R::op(ev, *h);
+        }
+        __syncwarp();
+        // the row open at the chunk start ends where the chunk's first non-empty row starts
+        if (lane == 0 && open_rid >= 0) {
+          const A v = val[col((unsigned)first_d)];
+          if (open_rid == hrow) {
+            p.head_row[w] = hrow;
+            p.head_part[w] = pack(v);
+          } else {
+            ((B*)p.out)[open_rid] = fin(v);
+          }
+        }
+        open_val = shfl_acc(sv, 31);
+        open_rid = r0 + last_put;
+      }
+      // finish the rows examined in this chunk that end inside it (value parked where the next row starts) and
+      // the empty ones; a row that ends at or after the chunk's end is the new open row
+      const int nrow = nxt - c0;
+      if (lane < nrow && eA < rhi_c) outw[c0 + lane] = fin(eA > dA ? val[col((unsigned)eA)] : R::id());
+      if (32 + lane < nrow && eB < rhi_c) outw[c0 + 32 + lane] = fin(eB > dB ? val[col((unsigned)eB)] : R::id());
+#pragma unroll 1
+      for (int j = 64 + lane; j < nrow; j += 32) {  // rows beyond the first 64: offsets re-read
+        const int64_t r = r0 + c0 + j;  // < rows
+        const int d = rel(__ldg(p.off + r));
+        const int e = rel(__ldg(p.off + r + 1));
+        if (e < rhi_c) outw[c0 + j] = fin(e > d ? val[col((unsigned)e)] : R::id());
+      }
+      __syncwarp();
+    }
+  }
+  // the row still open at hi
+  if (lane == 0 && open_rid >= 0) {
+    if (open_rid == hrow) {
+      p.head_row[w] = hrow;
+      p.head_part[w] = pack(open_val);
+    } else if (__ldg(p.off + open_rid + 1) <= hi) {
+      ((B*)p.out)[open_rid] = fin(open_val);
+    } else {
+      p.tail_row[w] = open_rid;
+      p.tail_part[w] = pack(open_val);
+    }
+  }
+  // the last warp also owns the empty rows that start at P1 (after every element)
+  if (w == nw - 1) {
+    const int64_t r = warp_lower_bound(p.off, rows, lo < hi ? P1 : lo);
+    for (int64_t q = r + lane; q < rows; q += 32)
+      if (__ldg(p.off + q) == __ldg(p.off + q + 1)) ((B*)p.out)[q] = fin(R::id());
+  }
+  cp_async_wait<0>();  // no copy may land in shared memory after the warp leaves
+}
+
 // ------------------------------------------------------------------------------------------ ragged, CTA tiles
 // The same clause and ownership rules as k_ragged_vec, with the CTA (not the warp) as the unit: CTA b owns the
 // element range [lo, hi) = [P0 + b*nnz/G, P0 + (b+1)*nnz/G) and every row whose first element lies in it, and

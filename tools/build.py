@@ -87,6 +87,23 @@ def build_ipm(force: bool = False, extra: list[str] | None = None) -> str:
 PTXAS_LOG = os.path.join(ROOT, "build", "ptxas_libipm.txt")
 
 
+def build_variant(tag: str, defines: list[str]) -> str:
+    """A/B build of libipm with extra -D flags into tools/bin/libipm_<tag>.so (travels to the GPU box; select it with
+    IPM_LIB=...). Its ptxas report goes to tools/bin/ptxas_<tag>.txt."""
+    nccl = _nccl_dir()
+    out = os.path.join(ROOT, "tools", "bin", f"libipm_{tag}.so")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    cus = [s for s in ipm_sources() if s.endswith(".cu")]
+    r = _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xptxas", "-v", "-Xcompiler", "-fPIC,-Wall",
+              "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nccl, "include"),
+              *[f"-D{d}" for d in defines], "-shared", "-o", out, *cus,
+              "-L", os.path.join(nccl, "lib"), "-l:libnccl.so.2", f"-Xlinker=-rpath={os.path.join(nccl, 'lib')}",
+              "-lcudart"])
+    with open(os.path.join(ROOT, "tools", "bin", f"ptxas_{tag}.txt"), "w") as f:
+        f.write(r.stdout + r.stderr)
+    return out
+
+
 def build_tools(force: bool = False) -> None:
     """Library-context timing program (CUB DeviceReduce) that bench.py's suite runs if present. Optional: a
     failure here does not fail the build."""
@@ -134,4 +151,7 @@ def build_all(force: bool = False) -> None:
 
 
 if __name__ == "__main__":
-    build_all(force="--force" in sys.argv)
+    if len(sys.argv) > 2 and sys.argv[1] == "variant":  # build.py variant TAG DEF=1 DEF2=3 ...
+        print(build_variant(sys.argv[2], sys.argv[3:]))
+    else:
+        build_all(force="--force" in sys.argv)

@@ -7,6 +7,10 @@ capture() {  # name kernel-regex command...
   ncu -i gpurun_out/prof_$name.ncu-rep --page source --csv --print-source sass > gpurun_out/ncu_${name}_sass.csv 2>/dev/null
   gzip -f gpurun_out/ncu_${name}_sass.csv; rm -f gpurun_out/prof_$name.ncu-rep
 }
-capture rtile_pl k_ragged_tile python tools/prof_ragged.py tile powerlaw
-capture rtile_c4k k_ragged_tile python tools/prof_ragged.py tile const4096
+# NCU=<kernel option name> (warp | tile | rank)
+case "$NCU" in
+  warp) K=k_ragged_vec ;; tile) K=k_ragged_tile ;; *) K=k_ragged_rank ;;
+esac
+capture r${NCU}_pl $K python tools/prof_ragged.py $NCU powerlaw
+capture r${NCU}_c4k $K python tools/prof_ragged.py $NCU const4096
 ls gpurun_out

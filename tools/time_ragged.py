@@ -8,9 +8,11 @@ from paper_1412_1127_b200 import ipm
 CASES = [("powerlaw", 1 << 24, 16.0), ("const", 1 << 22, 64.0), ("uniform", 1 << 24, 16.0),
          ("const", 1 << 16, 4096.0), ("const", 1 << 25, 4.0)]
 OPS = [("+", "float32"), ("max", "float32"), ("+", "float64"), ("^", "int32"), ("max", "float64")]
-KERNELS = ["warp", "tile"]
+KERNELS = os.environ.get("KERNELS", "warp,tile,rank").split(",")
 if len(sys.argv) > 1 and sys.argv[1] == "quick":
     OPS = OPS[:1]
+if os.environ.get("OPS"):  # e.g. OPS="+:float32,^:int32"
+    OPS = [tuple(o.split(":")) for o in os.environ["OPS"].split(",")]
 for kind, rows, mean in CASES:
     off = ipmgen.offsets_from_degrees(ipmgen.degrees(rows, seed=1, kind=kind, mean=mean))
     nnz = int(off[-1])
