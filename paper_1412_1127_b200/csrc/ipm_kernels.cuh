@@ -1503,7 +1503,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_ragged_tile(RaggedParams p) {
   __shared__ A s_wv[NW], s_red[NW];
   __shared__ long long s_wr[NW];
   __shared__ int s_wf[NW];
-  __shared__ int s_any[2];                // per tile parity: some row starts in the tile
+  __shared__ int s_any[3];                // per tile (mod 3): some row starts in the tile
   __shared__ A s_cv[2];                   // the row open at the end of the last flagged tile, and its id (by the
   __shared__ long long s_cr[2];           // parity q of flagged tiles: read in one, written for the next)
   __shared__ long long s_rs;
@@ -1521,7 +1521,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_ragged_tile(RaggedParams p) {
     if (lane == 0) s_rs = r0;
   }
   s_flag[t] = 0u;
-  if (t == 0) s_any[0] = s_any[1] = 0;
+  if (t == 0) s_any[0] = s_any[1] = s_any[2] = 0;
   __syncthreads();
   int64_t rs = s_rs;
   const int64_t hrow = (rs > 0 && lo < hi && __ldg(p.off + rs) > lo) ? rs - 1 : -1;  // spans lo from before
@@ -1568,7 +1568,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_ragged_tile(RaggedParams p) {
   };
   int par = 0;
 #pragma unroll 1
-  for (int64_t Bc = q0; Bc < hi; Bc += TILE, par ^= 1) {
+  for (int64_t Bc = q0; Bc < hi; Bc += TILE, par = par == 2 ? 0 : par + 1) {
     const int rlo = (int)(lo > Bc ? lo - Bc : 0);
     const int rhi = (int)(hi - Bc < TILE ? hi - Bc : TILE);
     const bool interior = rlo == 0 && rhi == TILE;  // CTA-uniform
@@ -1595,7 +1595,9 @@ __global__ void __launch_bounds__(BLOCK, MINB) k_ragged_tile(RaggedParams p) {
     }
     // (no barrier here: every thread cleared its own flag word when it read it, and the previous tile's readers of
     // s_rid / s_val / s_any finished before its last barrier)
-    if (t == 0) s_any[par ^ 1] = 0;  // the next tile's word (this tile's was cleared two tiles ago)
+    // the next tile's word: last read two tiles ago, before the previous tile's row-setup barrier (with two words
+    // a thread still reading the previous tile's word could race this store; racecheck, profiles/r02_san_*)
+    if (t == 0) s_any[par == 2 ? 0 : par + 1] = 0;
     // 1. row setup
 #pragma unroll 1
     while (true) {

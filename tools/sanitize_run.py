@@ -33,13 +33,22 @@ h = np.arange(100_000, dtype=np.int64)
 ipm.reduce_host("+", h)
 torch.cuda.synchronize()
 print("sanitize_run: ok")
-# ragged rows, several variables, 2-D region, the fused multi-rank exchange (2 ranks, one GPU)
+# ragged rows (all three kernels), several variables, 2-D region, the fused multi-rank exchange (2 ranks, one GPU)
+
+
+def ragged_all(op, x, off):
+    for kern in ("warp", "tile", "rank"):
+        ipm.set_option("ragged_kernel", kern)
+        ipm.reduce_ragged(op, x, off)
+    ipm.set_option("ragged_kernel", "auto")
+
+
 for dt in TD:
     off = np.array([0, 3, 3, 40, 41, 300, 300, 5000], np.int64) + 2
     x = torch.empty(int(off[-1]) + 3, dtype=TD[dt], device="cuda")
     ipmgen.fill_device(ipmgen.Spec(dt, x.numel(), "random", seed=2), x.data_ptr(), 0, x.numel(),
                        torch.cuda.current_stream().cuda_stream)
-    ipm.reduce_ragged("+", x, torch.from_numpy(off).cuda())
+    ragged_all("+", x, torch.from_numpy(off).cuda())
     for sig in ("sum_sumsq", "dot", "minmax", "stats"):
         ipm.reduce_fused(sig, x[1:2001], x[3:2003] if sig == "dot" else None)
     ipm.reduce_2d("max", x, rows=7, cols=300, row_stride=700)
@@ -49,13 +58,20 @@ for dt in TD:
     z = torch.empty(int(off2[-1]) + 1, dtype=TD[dt], device="cuda")
     ipmgen.fill_device(ipmgen.Spec(dt, z.numel(), "random", seed=4), z.data_ptr(), 0, z.numel(),
                        torch.cuda.current_stream().cuda_stream)
-    ipm.reduce_ragged("max", z[1:], torch.from_numpy(off2).cuda())
+    ragged_all("max", z[1:], torch.from_numpy(off2).cuda())
     # > 512 elements per warp: whole chunks in which no row starts (the flag-free path), rows across many warps
     off3 = np.array([0, 1_500_000, 1_500_003, 3_000_000, 3_000_000, 3_000_017, 4_600_000], np.int64) + 1
     z = torch.empty(int(off3[-1]) + 2, dtype=TD[dt], device="cuda")
     ipmgen.fill_device(ipmgen.Spec(dt, z.numel(), "random", seed=6), z.data_ptr(), 0, z.numel(),
                        torch.cuda.current_stream().cuda_stream)
-    ipm.reduce_ragged("+", z, torch.from_numpy(off3).cuda())
+    ragged_all("+", z, torch.from_numpy(off3).cuda())
+    # thousands of empty rows inside one chunk (jumps in the offset ring), more than 64 rows per chunk
+    d4 = np.ones(20_000, np.int64)
+    d4[100:6000] = 0
+    d4[7000] = 50_000
+    off4 = ipmgen.offsets_from_degrees(d4)
+    z = torch.empty(int(off4[-1]) + 1, dtype=TD[dt], device="cuda")
+    ragged_all("+", z, torch.from_numpy(off4).cuda())
     for rows, cols, stride in [(33, 1000, 1024), (5, 4099, 4101), (200, 31, 37)]:
         w = torch.empty(rows * stride + 1, dtype=TD[dt], device="cuda")
         ipmgen.fill_device(ipmgen.Spec(dt, w.numel(), "random", seed=5), w.data_ptr(), 0, w.numel(),
