@@ -236,7 +236,9 @@ typedef enum {
   IPM_OPT_DIST_TIMEOUT_MS = 4,  /* fused exchange: give up waiting for a peer after this long (default 30000) */
   IPM_OPT_RAGGED_KERNEL = 5     /* ragged rows: 0 auto (= 1), 1 one warp per element range (k_ragged_vec),
                                    2 one CTA per element range in tiles (k_ragged_tile),
-                                   3 one warp per element range with rank slots (k_ragged_rank) */
+                                   3 one warp per element range, rows finished in row order (k_ragged_rank),
+                                   4 one warp per element range, lane per row over shared-memory windows
+                                     (k_ragged_lpr) */
 } ipm_option;
 ipm_status ipm_set_option(ipm_option key, int64_t value);
 

@@ -274,6 +274,23 @@ struct Launch {
     k_ragged_rank<R, RR_WARPS, RR_MINB, RR_VPL, RR_NR, RR_PFV><<<blocks, RR_WARPS * 32, 0, st>>>(p);
     k_ragged_fix<R><<<(unsigned)((nw + 7) / 8), 256, 0, st>>>(p, nw);
   }
+  // lane-per-row ragged kernel: windows of <= 32 rows spanning <= LP_CAPB bytes staged in shared memory by cp.async
+#ifndef IPM_LP_WARPS
+#define IPM_LP_WARPS 4
+#endif
+#ifndef IPM_LP_MINB
+#define IPM_LP_MINB 8
+#endif
+#ifndef IPM_LP_CAPB
+#define IPM_LP_CAPB 4096
+#endif
+#ifndef IPM_LP_T
+#define IPM_LP_T 32
+#endif
+  static void ragged_lpr(const RaggedParams& p, int blocks, int64_t nw, cudaStream_t st) {
+    k_ragged_lpr<R, IPM_LP_WARPS, IPM_LP_MINB, IPM_LP_CAPB, 8, IPM_LP_T><<<blocks, IPM_LP_WARPS * 32, 0, st>>>(p);
+    k_ragged_fix<R><<<(unsigned)((nw + 7) / 8), 256, 0, st>>>(p, nw);
+  }
   // 8-byte folds run 3 CTAs x 256 per SM with up to 85 registers (+1-3 % over 4 CTAs at 64 registers; 4-byte folds
   // lose up to 17 % that way, profiles/r01_ab_2d_minb.txt). max_grid = SMs x the resident CTAs per SM.
   static constexpr int TWO_D_MINB = sizeof(typename R::B) == 8 ? 3 : 4;
@@ -312,6 +329,7 @@ struct Table {
   void (*ragged)(const RaggedParams&, int, int64_t, cudaStream_t);
   cudaError_t (*ragged_tile)(const RaggedParams&, int, cudaStream_t);
   void (*ragged_rank)(const RaggedParams&, int, int64_t, cudaStream_t);
+  void (*ragged_lpr)(const RaggedParams&, int, int64_t, cudaStream_t);
   int (*ragged_rank_ctas_per_sm)();
   void (*seg_warp)(const SegParams&, int, cudaStream_t);  // (params, SM count, stream)
   cudaError_t (*seg_tma)(const SegParams&, int, cudaStream_t);
@@ -323,7 +341,7 @@ struct Table {
 static const Table* table(ipm_op op, ipm_dtype dt) {
 #define IPM_ENTRY(O, D)                                                                                  \
   if (op == O && dt == D) {                                                                            \
-    static const Table t = {&Launch<O, D>::flat, &Launch<O, D>::two_d, &Launch<O, D>::ragged, &Launch<O, D>::ragged_tile, &Launch<O, D>::ragged_rank, &Launch<O, D>::ragged_rank_ctas_per_sm, &Launch<O, D>::seg_warp, &Launch<O, D>::seg_tma,     \
+    static const Table t = {&Launch<O, D>::flat, &Launch<O, D>::two_d, &Launch<O, D>::ragged, &Launch<O, D>::ragged_tile, &Launch<O, D>::ragged_rank, &Launch<O, D>::ragged_lpr, &Launch<O, D>::ragged_rank_ctas_per_sm, &Launch<O, D>::seg_warp, &Launch<O, D>::seg_tma,     \
                             &Launch<O, D>::seg_group, &Launch<O, D>::finalize, &Launch<O, D>::exchange};\
     return &t;                                                                                         \
   }
@@ -615,7 +633,7 @@ ipm_status ipm_set_option(ipm_option key, int64_t value) {
       g_opt_dist_timeout_ms = value;
       return IPM_OK;
     case IPM_OPT_RAGGED_KERNEL:
-      if (value < 0 || value > 3) break;
+      if (value < 0 || value > 4) break;
       g_opt_ragged_kernel = (int)value;
       return IPM_OK;
   }
@@ -911,7 +929,7 @@ ipm_status ipm_reduce_ragged(ipm_op op, ipm_dtype dt, const void* dev, const int
   const int kopt = g_opt_ragged_kernel.load(std::memory_order_relaxed);
   const int kern = kopt == 0 ? 1 : kopt;  // auto = the warp kernel (measured faster, profiles/r02_time_ragged_*)
   const Table* tb = table(op, dt);
-  const int64_t nw = kern == 1   ? std::min<int64_t>((int64_t)sm_count() * 32, WS_MAX_RAGGED_WARPS)  // 8 CTAs x 4 warps per SM
+  const int64_t nw = kern == 1 || kern == 4 ? std::min<int64_t>((int64_t)sm_count() * 32, WS_MAX_RAGGED_WARPS)  // 8 CTAs x 4 warps per SM
                      : kern == 3 ? (int64_t)std::min<int64_t>((int64_t)sm_count() * tb->ragged_rank_ctas_per_sm(),
                                                               WS_MAX_RAGGED_WARPS / IPM_RR_WARPS) *
                                            IPM_RR_WARPS  // one wave of CTAs
@@ -926,6 +944,7 @@ ipm_status ipm_reduce_ragged(ipm_op op, ipm_dtype dt, const void* dev, const int
     ProfScope ps(st, 4);
     if (kern == 1) tb->ragged(p, (int)(nw / 4), nw, st);
     else if (kern == 3) tb->ragged_rank(p, (int)(nw / IPM_RR_WARPS), nw, st);
+    else if (kern == 4) tb->ragged_lpr(p, (int)(nw / IPM_LP_WARPS), nw, st);
     else CK(tb->ragged_tile(p, (int)nw, st));
   }
   CK(cudaGetLastError());

@@ -1457,6 +1457,200 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_rank(RaggedParams p
   cp_async_wait<0>();  // no copy may land in shared memory after the warp leaves
 }
 
+// ------------------------------------------------------------------------------------------ ragged, lane per row
+// k_ragged_lpr: the ownership rules of k_ragged_vec (warp w owns the element range [lo, hi) and the rows that start
+// in it; head / tail records for the rows that cross its ends), with rows rather than elements as the lane unit
+// (round 2). Rows are taken in WINDOWS of up to 32 consecutive rows whose elements span at most CAPE elements
+// (the lanes read the window's offsets from a cp.async shared-memory ring, NR windows of 32 ahead); the window's
+// span is copied into shared memory with 16-byte cp.async (zero-filled past the span, no byte outside it read);
+// then each lane folds its own row from shared memory if it has at most T elements (one loop for the window,
+// maxlen steps), a longer row of the window is folded by the whole warp from shared memory (32 elements a step, a
+// warp reduction), and every lane stores its row's result: out[] is written by consecutive lanes. A row longer
+// than CAPE is a window of its own, folded by the whole warp from global memory with 32-byte loads. No flags, no
+// segmented scan: the work per element is one shared load and one op, the work per row one offset and one store.
+__device__ __forceinline__ void cp_async16z(void* s, const void* g, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(s)), "l"(g), "r"(src_bytes) : "memory");
+}
+
+template <class R, int WARPS, int MINB, int CAPB, int NR, int T>
+__global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_lpr(RaggedParams p) {
+  using B = typename R::B;
+  using A = typename R::A;
+  using VT = typename Vec<B>::T;
+  constexpr int VW = Vec<B>::W;
+  constexpr int CAPE = CAPB / (int)sizeof(B);  // elements per window span
+  constexpr int E16 = 16 / (int)sizeof(B);     // elements per 16-byte copy
+  constexpr int RING = 32 * NR;
+  static_assert(NR >= 4 && (NR & (NR - 1)) == 0, "offset ring: a power of two >= 4 windows");
+  static_assert(CAPB % 512 == 0, "span: whole 16-byte copies per lane");
+  __shared__ __align__(16) B s_stage[WARPS][CAPE + 2 * E16];  // the window's span, from a 16-byte aligned start
+  __shared__ int64_t s_off[WARPS][RING];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  B* stage = s_stage[wid];
+  int64_t* ring = s_off[wid];
+  const int64_t w = (int64_t)blockIdx.x * WARPS + wid;
+  const int64_t nw = (int64_t)gridDim.x * WARPS;
+  const B* a = (const B*)p.a;
+  const int64_t rows = p.rows;
+  const int64_t P0 = __ldg(p.off), P1 = __ldg(p.off + rows);
+  const int64_t nnz = P1 - P0;
+  const int64_t lo = P0 + (int64_t)(((__int128)nnz * w) / nw);
+  const int64_t hi = P0 + (int64_t)(((__int128)nnz * (w + 1)) / nw);
+  const int64_t r0 = warp_lower_bound(p.off, rows, lo);
+  const int64_t hrow = (r0 > 0 && lo < hi && __ldg(p.off + r0 - 1) < lo && __ldg(p.off + r0) > lo) ? r0 - 1 : -1;
+  const int nrel = (int)(rows - r0);
+  if (lane == 0) {
+    p.head_row[w] = lo < hi ? -1 : -2;
+    p.tail_row[w] = -1;
+  }
+  auto fin = [&](A v) { return R::fin(p.has_init ? R::op(R::lift((B)p.init), v) : v); };
+  // the whole warp folds a[s, e) from global memory: a scalar head to 32-byte alignment, 32-byte vectors (two in
+  // flight per lane), a scalar tail; the warp-reduced value (every lane)
+  auto fold_global = [&](int64_t s0, int64_t e0) -> A {
+    A v = R::id();
+    const int64_t head = ((32 - (int64_t)(((uintptr_t)(a + s0)) & 31u)) & 31) / (int64_t)sizeof(B);
+    const int64_t h1 = s0 + (head < e0 - s0 ? head : e0 - s0);
+    if (s0 + lane < h1) v = R::lift(lds(a + s0 + lane));
+    const VT* vp = (const VT*)(a + h1);
+    const int64_t nv = (e0 - h1) / VW;
+    using LC = Loc<R>;
+    typename LC::L la[VW];
+#pragma unroll
+    for (int k = 0; k < VW; ++k) la[k] = LC::id();
+    int64_t i = lane;
+#pragma unroll 1
+    for (; i + 32 < nv; i += 64) {
+      const VT t0 = ldv(vp + i), t1 = ldv(vp + i + 32);
+      LC::vec(la, t0);
+      LC::vec(la, t1);
+    }
+    if (i < nv) LC::vec(la, ldv(vp + i));
+#pragma unroll
+    for (int k = 1; k < VW; ++k) la[0] = LC::comb(la[0], la[k]);
+    v = R::op(v, LC::out(la[0]));
+    const int64_t t0 = h1 + nv * VW;
+    if (t0 + lane < e0) v = R::op(v, R::lift(lds(a + t0 + lane)));
+    return R::warp(v);
+  };
+  int nxt = 0;     // first row not yet taken, relative to r0
+  int issued = 0;  // offset windows issued (window j = rows r0 + 32j ..)
+  auto refill = [&]() {  // windows nxt/32 and nxt/32 + 1 complete, up to NR - 2 more in flight
+    const int bw = nxt >> 5;
+    if (issued < bw + NR) {
+      if (issued < bw + NR - 2) cp_async_wait<0>();  // a jump: no copy may still target a slot reused below
+      for (int j = issued > bw ? issued : bw; j < bw + NR; ++j) {
+        const int64_t r = r0 + 32 * (int64_t)j + lane;
+        cp_async8(&ring[32 * (j & (NR - 1)) + lane], p.off + (r < rows ? r : rows));
+        cp_async_commit();
+      }
+      issued = bw + NR;
+    }
+    cp_async_wait<NR - 2>();
+    __syncwarp();
+  };
+  if (lo < hi) {
+    // the row that started before lo: its elements in [lo, min(end, hi)) go to the head record
+    if (hrow >= 0) {
+      const int64_t e = __ldg(p.off + hrow + 1);
+      const A v = fold_global(lo, e < hi ? e : hi);
+      if (lane == 0) {
+        p.head_row[w] = hrow;
+        p.head_part[w] = pack(v);
+      }
+    }
+#pragma unroll 1
+    while (nxt < nrel) {
+      refill();
+      const int base = nxt & (RING - 1);
+      const int64_t s_i = ring[(base + lane) & (RING - 1)];   // start of row nxt + lane
+      const int64_t s_n = ring[(base + 32) & (RING - 1)];
+      const int64_t e_up = __shfl_down_sync(FULL, s_i, 1);
+      const int64_t e_raw = lane == 31 ? s_n : e_up;          // its end
+      const int64_t s0 = __shfl_sync(FULL, s_i, 0);
+      if (s0 >= hi) break;                                      // the rows from here on belong to later warps
+      const bool valid = nxt + lane < nrel && s_i < hi;
+      const int64_t e_i = e_raw < hi ? e_raw : hi;              // clipped to the warp's range
+      const int64_t len = valid ? e_i - s_i : 0;
+      const int64_t e0 = __shfl_sync(FULL, e_i, 0);
+      if (e0 - s0 > CAPE) {  // a long row: a window of its own, folded from global memory
+        const A v = fold_global(s0, e0);
+        if (lane == 0) {
+          const int64_t r = r0 + nxt;
+          if (e_raw > hi) {
+            p.tail_row[w] = r;
+            p.tail_part[w] = pack(v);
+          } else {
+            ((B*)p.out)[r] = fin(v);
+          }
+        }
+        ++nxt;
+        continue;
+      }
+      // the window: the leading rows whose span from s0 stays within CAPE elements
+      const bool inw = valid && e_i - s0 <= CAPE;
+      const unsigned wm = __ballot_sync(FULL, inw);
+      const int nwin = __popc(wm);  // a prefix of the lanes (>= 1: lane 0's row fits)
+      const int64_t ew = __shfl_sync(FULL, e_i, nwin - 1);
+      // stage [s0, ew) from the 16-byte aligned address at or below a + s0 (at most 12 bytes before the span, inside
+      // the same allocation: device allocations are 256-byte aligned); zero-filled past ew, nothing after it read
+      const int64_t sb = s0 - (int64_t)(((uintptr_t)(a + s0) & 15u) / sizeof(B));
+      const int nvec = (int)((ew - sb + E16 - 1) / E16);
+      for (int q = lane; q < nvec; q += 32) {
+        const int64_t g = sb + (int64_t)q * E16;
+        const int64_t rem = ew - g;
+        cp_async16z(stage + q * E16, a + g, (int)(rem < E16 ? rem : E16) * (int)sizeof(B));
+      }
+      cp_async_commit();
+      cp_async_wait<0>();
+      __syncwarp();
+      const int off_i = (int)(s_i - sb);
+      const int L = inw ? (int)len : 0;
+      const bool shrt = L <= T;
+      A v = R::id();
+      // short rows: lane per row
+      const int Ls = shrt ? L : 0;
+      const int maxl = __reduce_max_sync(FULL, Ls);
+      const B* sp = stage + off_i;
+#pragma unroll 1
+      for (int j = 0; j < maxl; j += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (j + u < Ls) v = R::op(v, R::lift(sp[j + u]));
+      }
+      // longer rows of the window: the whole warp from shared memory
+      unsigned mm = __ballot_sync(FULL, inw && !shrt);
+#pragma unroll 1
+      while (mm) {
+        const int ln = __ffs(mm) - 1;
+        mm &= mm - 1;
+        const int o = __shfl_sync(FULL, off_i, ln), n = __shfl_sync(FULL, L, ln);
+        A u = R::id();
+        for (int j = lane; j < n; j += 32) u = R::op(u, R::lift(stage[o + j]));
+        u = R::warp(u);
+        if (lane == ln) v = u;
+      }
+      if (inw) {
+        const int64_t r = r0 + nxt + lane;
+        if (e_raw > hi) {  // the row continues in the next warp's range
+          p.tail_row[w] = r;
+          p.tail_part[w] = pack(v);
+        } else {
+          ((B*)p.out)[r] = fin(v);
+        }
+      }
+      nxt += nwin;
+      __syncwarp();
+    }
+  }
+  // the last warp also owns the empty rows that start at P1 (after every element)
+  if (w == nw - 1) {
+    const int64_t r = warp_lower_bound(p.off, rows, lo < hi ? P1 : lo);
+    for (int64_t q = r + lane; q < rows; q += 32)
+      if (__ldg(p.off + q) == __ldg(p.off + q + 1)) ((B*)p.out)[q] = fin(R::id());
+  }
+  cp_async_wait<0>();
+}
+
 // ------------------------------------------------------------------------------------------ ragged, CTA tiles
 // The same clause and ownership rules as k_ragged_vec, with the CTA (not the warp) as the unit: CTA b owns the
 // element range [lo, hi) = [P0 + b*nnz/G, P0 + (b+1)*nnz/G) and every row whose first element lies in it, and

@@ -459,7 +459,7 @@ def identity_value(op: str, dt: int):
 
 OPTIONS = {"flat_ctas_per_sm": 0, "seg_kernel": 1, "deterministic": 2, "dist_mode": 3, "dist_timeout_ms": 4,
            "ragged_kernel": 5}
-RAGGED_KERNELS = {"auto": 0, "warp": 1, "tile": 2, "rank": 3}
+RAGGED_KERNELS = {"auto": 0, "warp": 1, "tile": 2, "rank": 3, "lpr": 4}
 DIST_MODES = {"auto": 0, "p2p": 0, "nccl": 1}
 SEG_KERNELS = {"auto": 0, "warp": 1, "ldg": 1, "tma": 2}
 

@@ -9,7 +9,7 @@ capture() {  # name kernel-regex command...
 }
 # NCU=<kernel option name> (warp | tile | rank)
 case "$NCU" in
-  warp) K=k_ragged_vec ;; tile) K=k_ragged_tile ;; *) K=k_ragged_rank ;;
+  warp) K=k_ragged_vec ;; tile) K=k_ragged_tile ;; lpr) K=k_ragged_lpr ;; *) K=k_ragged_rank ;;
 esac
 capture r${NCU}_pl $K python tools/prof_ragged.py $NCU powerlaw
 capture r${NCU}_c4k $K python tools/prof_ragged.py $NCU const4096
