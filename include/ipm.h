@@ -238,7 +238,8 @@ typedef enum {
                                    2 one CTA per element range in tiles (k_ragged_tile),
                                    3 one warp per element range, rows finished in row order (k_ragged_rank),
                                    4 one warp per element range, lane per row over shared-memory windows
-                                     (k_ragged_lpr) */
+                                     (k_ragged_lpr). Measured on one B200: 1 is the most even,
+                                     3 the fastest on short power-law rows, 4 on rows of >= 1K elements. */
 } ipm_option;
 ipm_status ipm_set_option(ipm_option key, int64_t value);
 
