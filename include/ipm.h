@@ -234,12 +234,15 @@ typedef enum {
   IPM_OPT_DETERMINISTIC = 2,
   IPM_OPT_DIST_MODE = 3,        /* 0 (default): fused peer-memory exchange when every peer is mapped; 1: NCCL */
   IPM_OPT_DIST_TIMEOUT_MS = 4,  /* fused exchange: give up waiting for a peer after this long (default 30000) */
-  IPM_OPT_RAGGED_KERNEL = 5     /* ragged rows: 0 auto (= 1), 1 one warp per element range (k_ragged_vec),
+  IPM_OPT_RAGGED_KERNEL = 5     /* ragged rows: 0 auto (1 below 256 elements per row on average over the whole
+                                   input, 128 for 8-byte types, else 4; both launched, the device picks, no host
+                                   sync),
+                                   1 one warp per element range (k_ragged_vec),
                                    2 one CTA per element range in tiles (k_ragged_tile),
                                    3 one warp per element range, rows finished in row order (k_ragged_rank),
                                    4 one warp per element range, lane per row over shared-memory windows
-                                     (k_ragged_lpr). Measured on one B200: 1 is the most even,
-                                     3 the fastest on short power-law rows, 4 on rows of >= 1K elements. */
+                                     (k_ragged_lpr). Measured on one B200: 1 the fastest on
+                                     rows of tens of elements, 3 on short power-law rows, 4 on rows of >= 256. */
 } ipm_option;
 ipm_status ipm_set_option(ipm_option key, int64_t value);
 

@@ -232,7 +232,7 @@ struct Launch {
     k_ragged_fix<R><<<(unsigned)((blocks + 7) / 8), 256, 0, st>>>(p, blocks);
     return cudaSuccess;
   }
-  static void ragged(const RaggedParams& p, int blocks, int64_t nw, cudaStream_t st) {
+  static void ragged_vec_only(const RaggedParams& p, int blocks, cudaStream_t st) {
     // 25 KiB of static shared memory per CTA: ask for the largest carveout so 8 CTAs fit on an SM
     // L2 prefetch of the next chunk (profiles/r01_sweep_ragged_5_l2prefetch.txt: +13-16 % on long rows, +1-7 % on
     // the power-law graph); for the widened float32 + * fold (issue-bound on short rows) only inside long rows
@@ -242,6 +242,9 @@ struct Launch {
                                                       (int)cudaSharedmemCarveoutMaxShared) == cudaSuccess;
     (void)carveout;
     k_ragged_vec<R, 4, 8, 2, true, PFV><<<blocks, 128, 0, st>>>(p);  // 8 CTAs x 4 warps per SM, 2 vectors per lane
+  }
+  static void ragged(const RaggedParams& p, int blocks, int64_t nw, cudaStream_t st) {
+    ragged_vec_only(p, blocks, st);
     k_ragged_fix<R><<<(unsigned)((nw + 7) / 8), 256, 0, st>>>(p, nw);
   }
   // rank-order ragged kernel: RR_WARPS warps per CTA, 2 vectors per lane, offset ring of RR_NR windows; as many CTAs
@@ -291,6 +294,22 @@ struct Launch {
     k_ragged_lpr<R, IPM_LP_WARPS, IPM_LP_MINB, IPM_LP_CAPB, 8, IPM_LP_T><<<blocks, IPM_LP_WARPS * 32, 0, st>>>(p);
     k_ragged_fix<R><<<(unsigned)((nw + 7) / 8), 256, 0, st>>>(p, nw);
   }
+  // auto: the warp kernel below RA_LONG elements per row on average (the whole input), the lane-per-row kernel at or
+  // above; both launched, the other one returns at once (gate on off[0], off[rows]). The crossover measured on one
+  // box (profiles/r02_time_ragged_cross.txt, rows of 128 .. 2048 elements): 256 elements for 4-byte types, 128 for
+  // 8-byte ones
+#ifndef IPM_RA_LONG
+#define IPM_RA_LONG (sizeof(typename R::B) == 8 ? 128 : 256)
+#endif
+  static void ragged_auto(const RaggedParams& p0, int blocks, int64_t nw, cudaStream_t st) {
+    RaggedParams p = p0;
+    p.gate_len = IPM_RA_LONG;
+    p.gate = 1;
+    ragged_vec_only(p, blocks, st);
+    p.gate = 2;
+    k_ragged_lpr<R, IPM_LP_WARPS, IPM_LP_MINB, IPM_LP_CAPB, 8, IPM_LP_T><<<blocks, IPM_LP_WARPS * 32, 0, st>>>(p);
+    k_ragged_fix<R><<<(unsigned)((nw + 7) / 8), 256, 0, st>>>(p, nw);
+  }
   // 8-byte folds run 3 CTAs x 256 per SM with up to 85 registers (+1-3 % over 4 CTAs at 64 registers; 4-byte folds
   // lose up to 17 % that way, profiles/r01_ab_2d_minb.txt). max_grid = SMs x the resident CTAs per SM.
   static constexpr int TWO_D_MINB = sizeof(typename R::B) == 8 ? 3 : 4;
@@ -330,6 +349,7 @@ struct Table {
   cudaError_t (*ragged_tile)(const RaggedParams&, int, cudaStream_t);
   void (*ragged_rank)(const RaggedParams&, int, int64_t, cudaStream_t);
   void (*ragged_lpr)(const RaggedParams&, int, int64_t, cudaStream_t);
+  void (*ragged_auto)(const RaggedParams&, int, int64_t, cudaStream_t);
   int (*ragged_rank_ctas_per_sm)();
   void (*seg_warp)(const SegParams&, int, cudaStream_t);  // (params, SM count, stream)
   cudaError_t (*seg_tma)(const SegParams&, int, cudaStream_t);
@@ -341,7 +361,7 @@ struct Table {
 static const Table* table(ipm_op op, ipm_dtype dt) {
 #define IPM_ENTRY(O, D)                                                                                  \
   if (op == O && dt == D) {                                                                            \
-    static const Table t = {&Launch<O, D>::flat, &Launch<O, D>::two_d, &Launch<O, D>::ragged, &Launch<O, D>::ragged_tile, &Launch<O, D>::ragged_rank, &Launch<O, D>::ragged_lpr, &Launch<O, D>::ragged_rank_ctas_per_sm, &Launch<O, D>::seg_warp, &Launch<O, D>::seg_tma,     \
+    static const Table t = {&Launch<O, D>::flat, &Launch<O, D>::two_d, &Launch<O, D>::ragged, &Launch<O, D>::ragged_tile, &Launch<O, D>::ragged_rank, &Launch<O, D>::ragged_lpr, &Launch<O, D>::ragged_auto, &Launch<O, D>::ragged_rank_ctas_per_sm, &Launch<O, D>::seg_warp, &Launch<O, D>::seg_tma,     \
                             &Launch<O, D>::seg_group, &Launch<O, D>::finalize, &Launch<O, D>::exchange};\
     return &t;                                                                                         \
   }
@@ -926,10 +946,12 @@ ipm_status ipm_reduce_ragged(ipm_op op, ipm_dtype dt, const void* dev, const int
   p.init = scalar_bits(dt, init);
   p.has_init = init != nullptr;
   p.out = dev_out;
+  p.gate = 0;
+  p.gate_len = 0;
   const int kopt = g_opt_ragged_kernel.load(std::memory_order_relaxed);
-  const int kern = kopt == 0 ? 1 : kopt;  // auto = the warp kernel (measured faster, profiles/r02_time_ragged_*)
+  const int kern = kopt;  // 0 auto: the warp kernel or, for long rows, the lane-per-row kernel (gated on device)
   const Table* tb = table(op, dt);
-  const int64_t nw = kern == 1 || kern == 4 ? std::min<int64_t>((int64_t)sm_count() * 32, WS_MAX_RAGGED_WARPS)  // 8 CTAs x 4 warps per SM
+  const int64_t nw = kern <= 1 || kern == 4 ? std::min<int64_t>((int64_t)sm_count() * 32, WS_MAX_RAGGED_WARPS)  // 8 CTAs x 4 warps per SM
                      : kern == 3 ? (int64_t)std::min<int64_t>((int64_t)sm_count() * tb->ragged_rank_ctas_per_sm(),
                                                               WS_MAX_RAGGED_WARPS / IPM_RR_WARPS) *
                                            IPM_RR_WARPS  // one wave of CTAs
@@ -942,9 +964,11 @@ ipm_status ipm_reduce_ragged(ipm_op op, ipm_dtype dt, const void* dev, const int
   cudaStream_t st = (cudaStream_t)stream;
   {
     ProfScope ps(st, 4);
-    if (kern == 1) tb->ragged(p, (int)(nw / 4), nw, st);
+    if (kern == 0) tb->ragged_auto(p, (int)(nw / 4), nw, st);
+    else if (kern == 1) tb->ragged(p, (int)(nw / 4), nw, st);
     else if (kern == 3) tb->ragged_rank(p, (int)(nw / IPM_RR_WARPS), nw, st);
     else if (kern == 4) tb->ragged_lpr(p, (int)(nw / IPM_LP_WARPS), nw, st);
+
     else CK(tb->ragged_tile(p, (int)nw, st));
   }
   CK(cudaGetLastError());

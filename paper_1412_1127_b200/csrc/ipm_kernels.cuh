@@ -882,6 +882,8 @@ struct RaggedParams {
   uint64_t* head_part;
   int64_t* tail_row;      // per warp: the owned row that continues into the next warp (-1: none)
   uint64_t* tail_part;
+  int gate;               // 0: run; 1: run only below gate_len elements per row on average; 2: only at or above
+  int64_t gate_len;
 };
 
 // first index r in [0, rows] with off[r] >= x (off non-decreasing); 32-ary search by the whole warp
@@ -921,8 +923,45 @@ __device__ __forceinline__ A shfl_acc(A v, int src) {
   return unpack<A>(__shfl_sync(FULL, pack(v), src));
 }
 
-template <class R, int WARPS, int MINB, int VPL, bool FF = true, int PFV = 0>
-__global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_vec(RaggedParams p) {
+// the ragged kernels' common prologue: warp w of nw owns the element range [lo, hi) of [P0, P1) and the rows that
+// start in it (r0: the first one), hrow is the row that crosses lo from before (-1: none); the warp's head / tail
+// records start empty (-2: an empty range, so the fix-up kernel passes over it)
+struct RaggedWarp {
+  int64_t w, nw, P1, lo, hi, r0, hrow;
+};
+// p.gate (0: none; 1: only below p.gate_len elements per row on average over the whole input; 2: only at or above):
+// false = this kernel does not run for this input and nothing is written. The lane-per-row kernel, idle on the
+// common short-row inputs, checks before the row search (EARLY_GATE: it returns after two loads); the warp kernel
+// after it (placed before it, ptxas spilled in the warp kernel's chunk loop)
+template <bool EARLY_GATE = false>
+__device__ __forceinline__ bool ragged_warp(RaggedWarp& g, const RaggedParams& p, int64_t w, int64_t nw) {
+  g.w = w;
+  g.nw = nw;
+  const int64_t P0 = __ldg(p.off);
+  g.P1 = __ldg(p.off + p.rows);
+  const int64_t nnz = g.P1 - P0;
+  if (EARLY_GATE && p.gate && (p.gate == 1) == (nnz >= p.gate_len * p.rows)) return false;
+  g.lo = P0 + (int64_t)(((__int128)nnz * w) / nw);
+  g.hi = P0 + (int64_t)(((__int128)nnz * (w + 1)) / nw);
+  g.r0 = warp_lower_bound(p.off, p.rows, g.lo);
+  g.hrow = (g.r0 > 0 && g.lo < g.hi && __ldg(p.off + g.r0 - 1) < g.lo && __ldg(p.off + g.r0) > g.lo) ? g.r0 - 1 : -1;
+  if (!EARLY_GATE && p.gate && (p.gate == 1) == (nnz >= p.gate_len * p.rows)) return false;
+  if ((threadIdx.x & 31) == 0) {
+    p.head_row[w] = g.lo < g.hi ? -1 : -2;
+    p.tail_row[w] = -1;
+  }
+  return true;
+}
+
+// per-warp shared memory of ragged_vec_body (one region per warp, carved below)
+template <class R, int VPL>
+struct RaggedVecSmem {
+  static constexpr int CH = 32 * Vec<typename R::B>::W * VPL;
+  static constexpr int BYTES = CH * (int)sizeof(int) + CH * (int)sizeof(typename R::A) + 32 * (int)sizeof(unsigned);
+};
+
+template <class R, int VPL, bool FF = true, int PFV = 0>
+__device__ __forceinline__ void ragged_vec_body(const RaggedParams& p, unsigned char* wsm, const RaggedWarp& g) {
   using B = typename R::B;
   using A = typename R::A;
   using VT = typename Vec<B>::T;
@@ -930,31 +969,22 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_vec(RaggedParams p)
   constexpr int EPL = VW * VPL;  // elements per lane per chunk (<= 32: one flag bit each)
   constexpr int CH = 32 * EPL;   // elements per chunk
   static_assert(EPL <= 32, "flag word");
-  // per warp, column-major by lane (position EPL*l + k at [k*32 + l]: a lane's column is bank-conflict free)
-  __shared__ int s_rid[WARPS][CH];        // chunk position -> (row - r0) starting there (valid where flagged)
-  __shared__ A s_val[WARPS][CH];          // value of the segment that ends just before a flagged position
-  __shared__ unsigned s_flag[WARPS][32];  // per lane: bit k = a row starts at the lane's element k
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int* rid_map = s_rid[wid];
-  const int* rid_col = s_rid[wid] + lane;
-  A* val_col = s_val[wid] + lane;
-  unsigned* flagw = s_flag[wid];
+  // per warp, column-major by lane (position EPL*l + k at [k*32 + l]: a lane's column is bank-conflict free):
+  // chunk position -> (row - r0) starting there (valid where flagged); the value of the segment that ends just
+  // before a flagged position; per lane, bit k = a row starts at the lane's element k
+  int* const s_rid = (int*)wsm;
+  A* const s_val = (A*)(wsm + CH * sizeof(int));
+  unsigned* const s_flag = (unsigned*)(wsm + CH * (sizeof(int) + sizeof(A)));
+  const int lane = threadIdx.x & 31;
+  int* rid_map = s_rid;
+  const int* rid_col = s_rid + lane;
+  A* val_col = s_val + lane;
+  unsigned* flagw = s_flag;
   flagw[lane] = 0u;
   const unsigned lanemask_lt = (1u << lane) - 1u;
-  const int64_t w = (int64_t)blockIdx.x * WARPS + wid;
-  const int64_t nw = (int64_t)gridDim.x * WARPS;
+  const int64_t w = g.w, nw = g.nw, P1 = g.P1, lo = g.lo, hi = g.hi, r0 = g.r0, hrow = g.hrow;
   const B* a = (const B*)p.a;
-  const int64_t P0 = __ldg(p.off), P1 = __ldg(p.off + p.rows);
-  const int64_t nnz = P1 - P0;
-  const int64_t lo = P0 + (int64_t)(((__int128)nnz * w) / nw);
-  const int64_t hi = P0 + (int64_t)(((__int128)nnz * (w + 1)) / nw);
   const bool last = (w == nw - 1);
-  const int64_t r0 = warp_lower_bound(p.off, p.rows, lo);
-  const int64_t hrow = (r0 > 0 && lo < hi && __ldg(p.off + r0 - 1) < lo && __ldg(p.off + r0) > lo) ? r0 - 1 : -1;
-  if (lane == 0) {
-    p.head_row[w] = lo < hi ? -1 : -2;
-    p.tail_row[w] = -1;
-  }
   auto finish = [&](int64_t row, A v) {  // a complete row owned by this warp
     if (p.has_init) v = R::op(R::lift((B)p.init), v);
     ((B*)p.out)[row] = R::fin(v);
@@ -1161,6 +1191,19 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_vec(RaggedParams p)
     for (int64_t q = r + lane; q < p.rows; q += 32)
       if (__ldg(p.off + q) == __ldg(p.off + q + 1)) finish(q, R::id());
   }
+}
+
+// auto (round 2): both the warp kernel and the lane-per-row kernel are launched; the mean row length of the whole
+// input, (off[rows] - off[0]) / rows, picks one of them and the other returns after two offset loads
+// (RaggedParams::gate, ragged_warp; profiles/r02_time_ragged_cross.txt)
+
+template <class R, int WARPS, int MINB, int VPL, bool FF = true, int PFV = 0>
+__global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_vec(RaggedParams p) {
+  __shared__ __align__(16) unsigned char sm[WARPS * RaggedVecSmem<R, VPL>::BYTES];
+  const int wid = threadIdx.x >> 5;
+  RaggedWarp g;
+  if (!ragged_warp(g, p, (int64_t)blockIdx.x * WARPS + wid, (int64_t)gridDim.x * WARPS)) return;
+  ragged_vec_body<R, VPL, FF, PFV>(p, sm + wid * RaggedVecSmem<R, VPL>::BYTES, g);
 }
 
 // one warp per phase-1 warp: a warp with a TAIL record finishes that row by folding the HEAD records of the
@@ -1472,8 +1515,16 @@ __device__ __forceinline__ void cp_async16z(void* s, const void* g, int src_byte
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(s)), "l"(g), "r"(src_bytes) : "memory");
 }
 
-template <class R, int WARPS, int MINB, int CAPB, int NR, int T>
-__global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_lpr(RaggedParams p) {
+// per-warp shared memory of ragged_lpr_body: the staged span (from a 16-byte aligned start), the offset ring
+template <class R, int CAPB, int NR>
+struct RaggedLprSmem {
+  static constexpr int E16 = 16 / (int)sizeof(typename R::B);
+  static constexpr int STAGE = (CAPB / (int)sizeof(typename R::B) + 2 * E16) * (int)sizeof(typename R::B);
+  static constexpr int BYTES = STAGE + 32 * NR * (int)sizeof(int64_t);
+};
+
+template <class R, int CAPB, int NR, int T>
+__device__ __forceinline__ void ragged_lpr_body(const RaggedParams& p, unsigned char* wsm, const RaggedWarp& g) {
   using B = typename R::B;
   using A = typename R::A;
   using VT = typename Vec<B>::T;
@@ -1483,26 +1534,13 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_lpr(RaggedParams p)
   constexpr int RING = 32 * NR;
   static_assert(NR >= 4 && (NR & (NR - 1)) == 0, "offset ring: a power of two >= 4 windows");
   static_assert(CAPB % 512 == 0, "span: whole 16-byte copies per lane");
-  __shared__ __align__(16) B s_stage[WARPS][CAPE + 2 * E16];  // the window's span, from a 16-byte aligned start
-  __shared__ int64_t s_off[WARPS][RING];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  B* stage = s_stage[wid];
-  int64_t* ring = s_off[wid];
-  const int64_t w = (int64_t)blockIdx.x * WARPS + wid;
-  const int64_t nw = (int64_t)gridDim.x * WARPS;
+  B* const stage = (B*)wsm;
+  int64_t* const ring = (int64_t*)(wsm + RaggedLprSmem<R, CAPB, NR>::STAGE);
+  const int lane = threadIdx.x & 31;
+  const int64_t w = g.w, nw = g.nw, P1 = g.P1, lo = g.lo, hi = g.hi, r0 = g.r0, hrow = g.hrow;
   const B* a = (const B*)p.a;
   const int64_t rows = p.rows;
-  const int64_t P0 = __ldg(p.off), P1 = __ldg(p.off + rows);
-  const int64_t nnz = P1 - P0;
-  const int64_t lo = P0 + (int64_t)(((__int128)nnz * w) / nw);
-  const int64_t hi = P0 + (int64_t)(((__int128)nnz * (w + 1)) / nw);
-  const int64_t r0 = warp_lower_bound(p.off, rows, lo);
-  const int64_t hrow = (r0 > 0 && lo < hi && __ldg(p.off + r0 - 1) < lo && __ldg(p.off + r0) > lo) ? r0 - 1 : -1;
   const int nrel = (int)(rows - r0);
-  if (lane == 0) {
-    p.head_row[w] = lo < hi ? -1 : -2;
-    p.tail_row[w] = -1;
-  }
   auto fin = [&](A v) { return R::fin(p.has_init ? R::op(R::lift((B)p.init), v) : v); };
   // the whole warp folds a[s, e) from global memory: a scalar head to 32-byte alignment, 32-byte vectors (two in
   // flight per lane), a scalar tail; the warp-reduced value (every lane)
@@ -1649,6 +1687,16 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_lpr(RaggedParams p)
       if (__ldg(p.off + q) == __ldg(p.off + q + 1)) ((B*)p.out)[q] = fin(R::id());
   }
   cp_async_wait<0>();
+}
+
+template <class R, int WARPS, int MINB, int CAPB, int NR, int T>
+__global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_lpr(RaggedParams p) {
+  static_assert(RaggedLprSmem<R, CAPB, NR>::BYTES % 16 == 0, "per-warp regions 16-byte aligned");
+  __shared__ __align__(16) unsigned char sm[WARPS * RaggedLprSmem<R, CAPB, NR>::BYTES];
+  const int wid = threadIdx.x >> 5;
+  RaggedWarp g;
+  if (!ragged_warp<true>(g, p, (int64_t)blockIdx.x * WARPS + wid, (int64_t)gridDim.x * WARPS)) return;
+  ragged_lpr_body<R, CAPB, NR, T>(p, sm + wid * RaggedLprSmem<R, CAPB, NR>::BYTES, g);
 }
 
 // ------------------------------------------------------------------------------------------ ragged, CTA tiles

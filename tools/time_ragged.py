@@ -9,6 +9,8 @@ CASES = [("powerlaw", 1 << 24, 16.0), ("const", 1 << 22, 64.0), ("uniform", 1 <<
          ("const", 1 << 16, 4096.0), ("const", 1 << 25, 4.0)]
 OPS = [("+", "float32"), ("max", "float32"), ("+", "float64"), ("^", "int32"), ("max", "float64")]
 KERNELS = os.environ.get("KERNELS", "warp,tile,rank").split(",")
+if os.environ.get("CASES"):  # e.g. CASES="const:262144:1024,powerlaw:16777216:16"
+    CASES = [(c.split(":")[0], int(c.split(":")[1]), float(c.split(":")[2])) for c in os.environ["CASES"].split(",")]
 if len(sys.argv) > 1 and sys.argv[1] == "quick":
     OPS = OPS[:1]
 if os.environ.get("OPS"):  # e.g. OPS="+:float32,^:int32"
