@@ -122,3 +122,29 @@ def test_c5_properties_and_prefix(ipm):
     comm = ipm.Comm(0, 1, torch.cuda.current_device(), store=dist.HashStore())
     assert comm.reduce("+", x) == full
     comm.close()
+
+
+# the bench suite's ragged graph (2^24 rows, power-law degrees, mean 16, 2.6e8 elements) and a long-row graph that
+# `auto` sends to the lane-per-row kernel, on every ragged kernel, element by element against the oracle
+def _ragged_graph(kind):
+    if kind == "powerlaw":
+        return ipmgen.offsets_from_degrees(ipmgen.degrees(1 << 24, seed=1, mean=16.0))
+    return ipmgen.offsets_from_degrees(ipmgen.degrees(1 << 16, seed=1, kind="const", mean=4096.0))
+
+
+@pytest.mark.parametrize("kern", ["auto", "warp", "rank", "lpr"])
+@pytest.mark.parametrize("kind", ["powerlaw", "const4096"])
+def test_ragged_fullsize(ipm, kind, kern):
+    off = _ragged_graph(kind)
+    spec = ipmgen.Spec("float32", int(off[-1]), "random", seed=1)
+    x = gen(spec)
+    offs = torch.from_numpy(off).cuda()
+    ipm.set_option("ragged_kernel", kern)
+    try:
+        got = ipm.reduce_ragged("+", x, offs).cpu().numpy()
+    finally:
+        ipm.set_option("ragged_kernel", "auto")
+    want_t, want_ld = oracle.reduce_ragged("+", x.cpu().numpy(), off)
+    # dyadic data on a 2^-14 grid, fp64 accumulation: every row sum is exact, so the result is the correctly
+    # rounded row sum, bit for bit
+    assert np.array_equal(got, want_t), (kind, kern)
