@@ -341,11 +341,14 @@ def suite(ipm, torch, ipmgen, peak):
     offs = torch.from_numpy(off).cuda()
     o = torch.empty(1 << 24, dtype=torch.float32, device="cuda")
     ms = timed(lambda: ipm.reduce_ragged("+", vals, offs, out=o, ws=ws))
-    med = statistics.median(ms)  # one record per call, covering both of its kernels
+    med = statistics.median(ms)  # one record per call, covering all of its kernels
     nbytes = nnz * 4 + off.size * 8 + (1 << 24) * 4
     out["ragged_float32_powerlaw_2^24rows"] = {"nnz": nnz, "max_degree": int(np.diff(off).max()),
                                                "ms_median": med, "GB/s": nbytes / med / 1e6,
-                                               "frac": nbytes / med / 1e6 / peak, "kernels_per_call": 2}
+                                               "frac": nbytes / med / 1e6 / peak, "kernel": "auto",
+                                               "kernels_per_call": 3,
+                                               "kernels_note": "k_ragged_vec (runs: mean row length 16 < 256), "
+                                                               "k_ragged_lpr (returns after its gate), k_ragged_fix"}
     del vals, offs, o
     torch.cuda.empty_cache()
     # library context: CUB's DeviceReduce / DeviceSegmentedReduce on the same shapes, including this ragged graph
