@@ -447,6 +447,15 @@ ipm_status launch_exchange(ipm_op op, ipm_dtype dt, const uint64_t* acc, uint64_
 }
 
 // ------------------------------------------------------------------------------------------ fused
+// 32-byte vectors per thread per tile: 4 for one stream, 2 per stream for two (x*y); same-box A/B
+// (profiles/r02_ab_fused_u.txt): one stream at U = 4 vs 2 +1.2 % (float32 stats) .. +6.6 % (float64 stats), x*y at
+// U = 4 -4 %; U = 6 / 8 no better (r02_ab_fused_u1.txt)
+#ifndef IPM_FUSED_U1
+#define IPM_FUSED_U1 4
+#endif
+#ifndef IPM_FUSED_U2
+#define IPM_FUSED_U2 2
+#endif
 template <int DT>
 struct FusedLaunch {
   using ADDX = Comp<Red<IPM_ADD, DT>, EX>;
@@ -457,8 +466,10 @@ struct FusedLaunch {
   template <class C0, class C1, class C2, class C3, bool TWO>
   static void go(const FusedParams& p, bool vec, int grid, cudaStream_t st) {
     using S = Sig<C0, C1, C2, C3>;
-    if (vec) k_fused<S, C0, C1, C2, C3, TWO, true, FLAT_BLOCK, 2><<<grid, FLAT_BLOCK, 0, st>>>(p);
-    else k_fused<S, C0, C1, C2, C3, TWO, false, FLAT_BLOCK, 2><<<grid, FLAT_BLOCK, 0, st>>>(p);
+    // int64 keeps U = 2 for one stream too: its 64-bit x*x products at U = 4 spill (ptxas)
+    constexpr int U = TWO || DT == IPM_I64 ? IPM_FUSED_U2 : IPM_FUSED_U1;
+    if (vec) k_fused<S, C0, C1, C2, C3, TWO, true, FLAT_BLOCK, U><<<grid, FLAT_BLOCK, 0, st>>>(p);
+    else k_fused<S, C0, C1, C2, C3, TWO, false, FLAT_BLOCK, U><<<grid, FLAT_BLOCK, 0, st>>>(p);
   }
   static void launch(ipm_fused f, const FusedParams& p, bool vec, int grid, cudaStream_t st) {
     switch (f) {

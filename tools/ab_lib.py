@@ -8,7 +8,8 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CASES = [("flat", "float32", "+", 1 << 28), ("flat", "float64", "max", 1 << 28), ("flat", "int64", "&&", 1 << 30),
          ("seg", "float32", "+", 65536 * 4096), ("2d", "float32", "+", 16384 * 16384),
-         ("stats", "float32", "+", 1 << 28), ("2d", "float32", "max", 16384 * 16384), ("2d", "int32", "^", 16384 * 16384),
+         ("stats", "float32", "+", 1 << 28), ("sum_sumsq", "float32", "+", 1 << 28), ("minmax", "float32", "+", 1 << 28),
+         ("dot", "float32", "+", 1 << 29), ("stats", "float64", "+", 1 << 28), ("2d", "float32", "max", 16384 * 16384), ("2d", "int32", "^", 16384 * 16384),
          ("2d", "float64", "+", 16384 * 16384), ("seg", "float32", "max", 65536 * 4096),
          ("seg", "float64", "+", 65536 * 4096), ("seg", "int32", "^", 65536 * 4096), ("seg", "int64", "min", 65536 * 4096),
          ("2d", "int32", "+", 16384 * 16384), ("2d", "int64", "+", 8192 * 16384), ("2d", "int64", "max", 8192 * 16384),
@@ -40,8 +41,10 @@ def child():
                 ipm.reduce_segmented(op, x.view(65536, 4096))
             elif kind == "2d":
                 ipm.reduce_2d(op, x.view(-1, 16384)[:, :16000])
+            elif kind == "dot":
+                ipm.reduce_fused_async("dot", x[: n // 2], x[n // 2:])
             else:
-                ipm.reduce_fused_async("stats", x)
+                ipm.reduce_fused_async(kind, x)
         t0 = time.perf_counter()
         while time.perf_counter() - t0 < 0.2:
             call()
