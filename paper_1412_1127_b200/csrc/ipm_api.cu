@@ -408,6 +408,7 @@ ipm_status launch_flat(ipm_op op, ipm_dtype dt, const void* dev, int64_t n, uint
   p.partials = (uint64_t*)((char*)ws + WS_PARTIALS);
   p.tickets = (unsigned*)((char*)ws + WS_TICKETS);
   p.counter = (unsigned long long*)((char*)ws + WS_COUNTER);
+  p.packed = (unsigned long long*)((char*)ws + WS_PACKED);
   const int64_t grid = flat_grid(dt, n);
   p.max_chunks = std::max<int64_t>(1, WS_MAX_PARTIALS - grid - 1);
   p.peers = dist ? dist->peers : nullptr;
@@ -834,6 +835,7 @@ ipm_status ipm_reduce_segmented(ipm_op op, ipm_dtype dt, const void* dev, int64_
     p.partials = ws ? (uint64_t*)((char*)ws + WS_PARTIALS) : nullptr;
     p.tickets = ws ? (unsigned*)((char*)ws + WS_TICKETS) : nullptr;
     p.counter = nullptr;
+    p.packed = nullptr;
     p.max_chunks = 0;
     p.peers = nullptr;
     p.rank = 0;
@@ -897,6 +899,7 @@ ipm_status ipm_reduce_partials(ipm_op op, ipm_dtype dt, const void* dev, int64_t
   p.partials = nullptr;
   p.tickets = nullptr;
   p.counter = nullptr;
+  p.packed = nullptr;
   p.max_chunks = 0;
   p.peers = nullptr;
   p.rank = 0;
@@ -1027,6 +1030,7 @@ ipm_status ipm_reduce_2d_async(ipm_op op, ipm_dtype dt, const void* dev, int64_t
   q.f.partials = (uint64_t*)((char*)ws + WS_PARTIALS);
   q.f.tickets = (unsigned*)((char*)ws + WS_TICKETS);
   q.f.counter = nullptr;
+  q.f.packed = (unsigned long long*)((char*)ws + WS_PACKED);
   q.f.max_chunks = 0;
   q.f.peers = nullptr;
   q.f.rank = 0;

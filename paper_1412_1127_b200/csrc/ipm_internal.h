@@ -14,6 +14,7 @@ constexpr size_t WS_RESULT = 4096;        // result slots (up to 4 elements of 8
 constexpr size_t WS_LOCAL = 4160;         // this rank's accumulator partial (multi-GPU)
 constexpr size_t WS_ACC = 4224;           // running accumulator (host-streaming path)
 constexpr size_t WS_COUNTER = 4288;       // dynamic tile counter of the flat kernel (left at zero)
+constexpr size_t WS_PACKED = 4296;        // int32 + count-and-sum word of the static flat kernel (left at zero)
 constexpr size_t WS_SLOTS = 4352;         // gathered partials, one per rank
 constexpr int WS_MAX_RANKS = 64;
 constexpr size_t WS_PARTIALS = 8192;      // per-CTA partials

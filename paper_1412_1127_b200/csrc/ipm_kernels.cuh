@@ -15,6 +15,7 @@
 //   k_seg_group the same for short rows: a group of G <= 32 lanes per row
 //   k_finalize  fold of P accumulator slots (cross-rank, or cross-chunk) + init, rounding to T (a6/a9)
 #pragma once
+#include <type_traits>
 #include "ipm_ops.cuh"
 
 namespace ipm {
@@ -98,6 +99,8 @@ struct FlatParams {
   uint64_t* partials;     // gridDim.x * gridDim.y slots (unused when gridDim.x == 1)
   unsigned* tickets;      // gridDim.y tickets (unused when gridDim.x == 1); left at zero
   unsigned long long* counter;  // dynamic schedules: tile / chunk counter, left at zero
+  unsigned long long* packed;   // int32 +, one row: the CTA count (low word) and the wrapping sum (high word) in
+                                // one 64-bit word, left at zero (nullptr: not used)
   int64_t max_chunks;     // k_flat_guided: partial slots available for dynamic chunks
   // MODE_DIST (multi-GPU, one kernel): the CTA that finishes this rank's shard exchanges the rank partial with
   // every peer through NVLink peer memory (see dist_exchange)
@@ -236,6 +239,23 @@ __device__ __forceinline__ void grid_finish(const FlatParams& p, int64_t row, ty
       if (p.counter) *p.counter = 0ull;  // (the single CTA has finished claiming tiles)
     }
     return;
+  }
+  if constexpr (std::is_same<R, Red<IPM_ADD, IPM_I32>>::value) {
+    // int32 + (BASELINE config 1): the CTA's partial rides in the ticket itself, count in the low word and the sum
+    // mod 2^32 in the high word of one 64-bit atomic (the count never carries into the sum: at most 2^31 CTAs),
+    // so the last CTA has the total without storing and re-loading partials or a CTA reduction: one L2 round trip
+    // fewer on the latency-bound small inputs (profiles/r02_c1_breakdown.txt). The sum is exact in any order.
+    if (p.packed && gridDim.y == 1) {
+      if (threadIdx.x == 0) {
+        const unsigned long long old = atomicAdd(p.packed, ((unsigned long long)cta << 32) | 1ull);
+        if ((unsigned)old == gridDim.x - 1) {
+          *p.packed = 0ull;
+          if (p.counter) *p.counter = 0ull;
+          store_out<R>(p, row, (A)(old >> 32) + cta);
+        }
+      }
+      return;
+    }
   }
   uint64_t* parts = p.partials + row * gridDim.x;
   if (threadIdx.x == 0) {
