@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -395,7 +396,8 @@ static ipm_status check_array(ipm_dtype dt, const void* dev, int64_t n) {
 }
 
 ipm_status launch_flat(ipm_op op, ipm_dtype dt, const void* dev, int64_t n, uint64_t init, int has_init, int mode,
-                       void* out, void* ws, cudaStream_t st, const DistArgs* dist) {
+                       void* out, void* ws, cudaStream_t st, const DistArgs* dist, unsigned long long* done,
+                       unsigned long long done_seq) {
   const Table* t = table(op, dt);
   FlatParams p;
   p.a = dev;
@@ -409,6 +411,8 @@ ipm_status launch_flat(ipm_op op, ipm_dtype dt, const void* dev, int64_t n, uint
   p.tickets = (unsigned*)((char*)ws + WS_TICKETS);
   p.counter = (unsigned long long*)((char*)ws + WS_COUNTER);
   p.packed = (unsigned long long*)((char*)ws + WS_PACKED);
+  p.done = mode == MODE_RESULT ? done : nullptr;
+  p.done_seq = done_seq;
   const int64_t grid = flat_grid(dt, n);
   p.max_chunks = std::max<int64_t>(1, WS_MAX_PARTIALS - grid - 1);
   p.peers = dist ? dist->peers : nullptr;
@@ -571,6 +575,7 @@ namespace {
 struct Mailbox {
   void* host[64] = {nullptr};
   void* dev[64] = {nullptr};
+  unsigned long long seq[64] = {0};  // the last done flag value asked of a kernel (word 1 of the buffer)
 };
 thread_local Mailbox tl_mail;
 }  // namespace
@@ -585,6 +590,7 @@ ipm_status result_mailbox(void** host, void** dev) {
   if (!tl_mail.host[d]) {
     void* h = nullptr;
     CK(cudaHostAlloc(&h, 64, cudaHostAllocMapped | cudaHostAllocPortable));
+    memset(h, 0, 64);  // word 1 is the done flag: no stale value may match a sequence number
     void* dp = nullptr;
     cudaError_t e = cudaHostGetDevicePointer(&dp, h, 0);
     if (e != cudaSuccess) {
@@ -596,6 +602,34 @@ ipm_status result_mailbox(void** host, void** dev) {
   }
   *host = tl_mail.host[d];
   *dev = tl_mail.dev[d];
+  return IPM_OK;
+}
+
+// the next done-flag value for this thread's mailbox on the current device (result_mailbox called first)
+unsigned long long mailbox_next_seq() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return ++tl_mail.seq[d];
+}
+
+// Wait for a synchronous call's result: poll the mailbox's done flag (the kernel stores it with system-scope
+// release after the result, so the result is visible once the flag is), at most POLL_NS, then fall back to a stream
+// synchronize (long kernels, and errors: a failed kernel never sets the flag). Polling skips the driver's wake-up
+// path of cudaStreamSynchronize on the latency-bound small calls (BASELINE config 1).
+ipm_status wait_mailbox(void* host, unsigned long long seq, cudaStream_t st) {
+  constexpr long long POLL_NS = 200000;
+  volatile unsigned long long* flag = (volatile unsigned long long*)host + 1;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int i = 0;; ++i) {
+    if (__atomic_load_n((const unsigned long long*)flag, __ATOMIC_ACQUIRE) == seq) return IPM_OK;
+    if ((i & 255) == 255 &&
+        std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count() > POLL_NS)
+      break;
+#if defined(__x86_64__)
+    __builtin_ia32_pause();
+#endif
+  }
+  CK(cudaStreamSynchronize(st));
   return IPM_OK;
 }
 }  // namespace ipm
@@ -780,8 +814,17 @@ ipm_status ipm_reduce(ipm_op op, ipm_dtype dt, const void* dev, int64_t n, void*
   void *mh, *md;
   ipm_status s = result_mailbox(&mh, &md);
   if (s) return s;
-  if ((s = ipm_reduce_async(op, dt, dev, n, inout, md, ws, stream))) return s;
-  CK(cudaStreamSynchronize((cudaStream_t)stream));  // end of the compute region
+  if (n > 0) {  // the flat kernel signals the mailbox: poll it (end of the compute region)
+    if ((s = validate(op, dt)) || (s = check_array(dt, dev, n)) || (s = check_ws(ws))) return s;
+    const unsigned long long seq = mailbox_next_seq();
+    if ((s = launch_flat(op, dt, dev, n, scalar_bits(dt, inout), 1, MODE_RESULT, md, ws, (cudaStream_t)stream,
+                         nullptr, (unsigned long long*)md + 1, seq)))
+      return s;
+    if ((s = wait_mailbox(mh, seq, (cudaStream_t)stream))) return s;
+  } else {
+    if ((s = ipm_reduce_async(op, dt, dev, n, inout, md, ws, stream))) return s;
+    CK(cudaStreamSynchronize((cudaStream_t)stream));
+  }
   memcpy(inout, mh, esize(dt));
   return IPM_OK;
 }
@@ -836,6 +879,7 @@ ipm_status ipm_reduce_segmented(ipm_op op, ipm_dtype dt, const void* dev, int64_
     p.tickets = ws ? (unsigned*)((char*)ws + WS_TICKETS) : nullptr;
     p.counter = nullptr;
     p.packed = nullptr;
+    p.done = nullptr;
     p.max_chunks = 0;
     p.peers = nullptr;
     p.rank = 0;
@@ -900,6 +944,7 @@ ipm_status ipm_reduce_partials(ipm_op op, ipm_dtype dt, const void* dev, int64_t
   p.tickets = nullptr;
   p.counter = nullptr;
   p.packed = nullptr;
+  p.done = nullptr;
   p.max_chunks = 0;
   p.peers = nullptr;
   p.rank = 0;
@@ -1031,6 +1076,7 @@ ipm_status ipm_reduce_2d_async(ipm_op op, ipm_dtype dt, const void* dev, int64_t
   q.f.tickets = (unsigned*)((char*)ws + WS_TICKETS);
   q.f.counter = nullptr;
   q.f.packed = (unsigned long long*)((char*)ws + WS_PACKED);
+  q.f.done = nullptr;
   q.f.max_chunks = 0;
   q.f.peers = nullptr;
   q.f.rank = 0;

@@ -43,7 +43,8 @@ struct DistArgs {             // L_DIST: the fused multi-GPU exchange (ipm_kerne
   long long timeout_ns;
 };
 ipm_status launch_flat(ipm_op op, ipm_dtype dt, const void* dev, int64_t n, uint64_t init, int has_init, int mode,
-                       void* out, void* ws, cudaStream_t st, const DistArgs* dist = nullptr);
+                       void* out, void* ws, cudaStream_t st, const DistArgs* dist = nullptr,
+                       unsigned long long* done = nullptr, unsigned long long done_seq = 0);
 ipm_status launch_exchange(ipm_op op, ipm_dtype dt, const uint64_t* acc, uint64_t init, int has_init, void* out,
                            const DistArgs* dist, cudaStream_t st);
 // host-streaming copyin fused with the reduction: leaves the accumulator partial of host[0..n) at ws + WS_ACC

@@ -101,6 +101,8 @@ struct FlatParams {
   unsigned long long* counter;  // dynamic schedules: tile / chunk counter, left at zero
   unsigned long long* packed;   // int32 +, one row: the CTA count (low word) and the wrapping sum (high word) in
                                 // one 64-bit word, left at zero (nullptr: not used)
+  unsigned long long* done;     // MODE_RESULT: after the result, done_seq is stored here with system-scope release
+  unsigned long long done_seq;  // (the synchronous call's mapped mailbox: the host polls it; nullptr: not used)
   int64_t max_chunks;     // k_flat_guided: partial slots available for dynamic chunks
   // MODE_DIST (multi-GPU, one kernel): the CTA that finishes this rank's shard exchanges the rank partial with
   // every peer through NVLink peer memory (see dist_exchange)
@@ -195,6 +197,7 @@ __device__ __forceinline__ void store_out(const FlatParams& p, int64_t row, type
       A t = total;
       if (p.has_init) t = R::op(R::lift((B)p.init), total);  // var = var_original ⊕ fold (R1)
       ((B*)p.out)[row] = R::fin(t);
+      if (p.done) st_release_sys((uint64_t*)p.done, p.done_seq);  // the result first, then the flag
       break;
     }
     case MODE_PARTIAL: ((uint64_t*)p.out)[row] = pack(total); break;
