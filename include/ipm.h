@@ -193,6 +193,22 @@ ipm_status ipm_reduce_fused_async(ipm_fused f, ipm_dtype dt, const void* x, cons
 ipm_status ipm_reduce_ragged(ipm_op op, ipm_dtype dt, const void* dev, const int64_t* dev_offsets, int64_t rows,
                              const void* init, void* dev_out, void* workspace, void* stream);
 
+/* The same clause (identical results, bit for bit on every (op, dtype): the fold of each row is split at the
+ * same element positions as in ipm_reduce_ragged's default kernel), computed in two passes over caller-owned
+ * scratch: a row-parallel pass marks where every row starts in a bitmap over the elements, counts the row starts
+ * per chunk of 512 elements (256 for 8-byte types) and writes every EMPTY row (init ⊕ identity); an
+ * element-parallel pass then folds the elements, reading each lane's row-start flags from the bitmap and naming
+ * rows by rank within their chunk instead of walking the row offsets per chunk.
+ * nvalues: the element array's length, >= off[rows] (the bound the scratch is sized from).
+ * scratch: 256-byte aligned device buffer of at least ipm_ragged_scratch_bytes(dt, nvalues) bytes, caller-owned;
+ *   its contents on entry do not matter (the library zeroes it in stream order); not used after the call's
+ *   kernels complete. Too small -> IPM_E_WORKSPACE; misaligned -> IPM_E_ALIGN.
+ * Four launches on `stream` (memset, mark, fold, fix-up); workspace as for ipm_reduce_ragged. */
+size_t ipm_ragged_scratch_bytes(ipm_dtype dt, int64_t nvalues);
+ipm_status ipm_reduce_ragged_marked(ipm_op op, ipm_dtype dt, const void* dev, int64_t nvalues,
+                                    const int64_t* dev_offsets, int64_t rows, const void* init, void* dev_out,
+                                    void* workspace, void* scratch, size_t scratch_bytes, void* stream);
+
 /* End-to-end clause over a HOST array: the data clause `copyin(a[0:n])` fused with the reduction. The host
  * array is streamed to the device in chunks through two library-owned staging buffers (allocated once
  * through the allocator hook and kept until ipm_release_staging), each chunk's H2D copy overlapping the

@@ -311,6 +311,39 @@ struct Launch {
     k_ragged_lpr<R, IPM_LP_WARPS, IPM_LP_MINB, IPM_LP_CAPB, 8, IPM_LP_T><<<blocks, IPM_LP_WARPS * 32, 0, st>>>(p);
     k_ragged_fix<R><<<(unsigned)((nw + 7) / 8), 256, 0, st>>>(p, nw);
   }
+  // marked rows (two passes, k_ragged_mark + k_ragged_mk, then the fix-up): chunks of 512 elements (4-byte) / 256
+  // (8-byte), 8 CTAs x 4 warps per SM; the scratch (bitmap + chunk counts) is zeroed in stream order first
+  // widened folds (float32 + *: float64 accumulators) 4 vectors per lane at 6 CTAs per SM, the others 2 at 8; every
+  // fold asks L2 for the chunk after the next (profiles/r02_ab_marked_1.txt)
+  static constexpr bool MK_WIDE = sizeof(typename R::A) > sizeof(typename R::B);
+#ifndef IPM_MK_VPL
+#define IPM_MK_VPL (MK_WIDE ? 4 : 2)
+#endif
+#ifndef IPM_MK_MINB
+#define IPM_MK_MINB (MK_WIDE ? 6 : 8)
+#endif
+#ifndef IPM_MK_PFD
+#define IPM_MK_PFD 1
+#endif
+  static constexpr int MK_VPL = IPM_MK_VPL, MK_MINB = IPM_MK_MINB, MK_PFD = IPM_MK_PFD;
+  static int64_t ragged_mk_warps(int sms) {
+    return std::min<int64_t>((int64_t)sms * 4 * MK_MINB, WS_MAX_RAGGED_WARPS);  // one wave of 4-warp CTAs
+  }
+  static constexpr int MK_CH = 32 * Vec<typename R::B>::W * MK_VPL;
+  static cudaError_t ragged_mk(const RaggedParams& p, const RaggedMarks& m, size_t zero_bytes, int sms, int64_t nw,
+                               cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(m.bits, 0, zero_bytes, st);
+    if (e != cudaSuccess) return e;
+    const int64_t blocks0 = std::min<int64_t>((p.rows + 1023) / 1024, (int64_t)sms * 8);  // 8 warps x 128 rows
+    k_ragged_mark<R, MK_CH><<<(unsigned)blocks0, 256, 0, st>>>(p, m);
+    static const bool carveout = cudaFuncSetAttribute(k_ragged_mk<R, 4, MK_MINB, MK_VPL, MK_PFD>,
+                                                      cudaFuncAttributePreferredSharedMemoryCarveout,
+                                                      (int)cudaSharedmemCarveoutMaxShared) == cudaSuccess;
+    (void)carveout;
+    k_ragged_mk<R, 4, MK_MINB, MK_VPL, MK_PFD><<<(unsigned)(nw / 4), 128, 0, st>>>(p, m);
+    k_ragged_fix<R><<<(unsigned)((nw + 7) / 8), 256, 0, st>>>(p, nw);
+    return cudaSuccess;
+  }
   // 8-byte folds run 3 CTAs x 256 per SM with up to 85 registers (+1-3 % over 4 CTAs at 64 registers; 4-byte folds
   // lose up to 17 % that way, profiles/r01_ab_2d_minb.txt). max_grid = SMs x the resident CTAs per SM.
   static constexpr int TWO_D_MINB = sizeof(typename R::B) == 8 ? 3 : 4;
@@ -352,6 +385,8 @@ struct Table {
   void (*ragged_lpr)(const RaggedParams&, int, int64_t, cudaStream_t);
   void (*ragged_auto)(const RaggedParams&, int, int64_t, cudaStream_t);
   int (*ragged_rank_ctas_per_sm)();
+  cudaError_t (*ragged_mk)(const RaggedParams&, const RaggedMarks&, size_t, int, int64_t, cudaStream_t);
+  int64_t (*ragged_mk_warps)(int);
   void (*seg_warp)(const SegParams&, int, cudaStream_t);  // (params, SM count, stream)
   cudaError_t (*seg_tma)(const SegParams&, int, cudaStream_t);
   void (*seg_group)(const SegParams&, int, int, cudaStream_t);
@@ -362,7 +397,7 @@ struct Table {
 static const Table* table(ipm_op op, ipm_dtype dt) {
 #define IPM_ENTRY(O, D)                                                                                  \
   if (op == O && dt == D) {                                                                            \
-    static const Table t = {&Launch<O, D>::flat, &Launch<O, D>::two_d, &Launch<O, D>::ragged, &Launch<O, D>::ragged_tile, &Launch<O, D>::ragged_rank, &Launch<O, D>::ragged_lpr, &Launch<O, D>::ragged_auto, &Launch<O, D>::ragged_rank_ctas_per_sm, &Launch<O, D>::seg_warp, &Launch<O, D>::seg_tma,     \
+    static const Table t = {&Launch<O, D>::flat, &Launch<O, D>::two_d, &Launch<O, D>::ragged, &Launch<O, D>::ragged_tile, &Launch<O, D>::ragged_rank, &Launch<O, D>::ragged_lpr, &Launch<O, D>::ragged_auto, &Launch<O, D>::ragged_rank_ctas_per_sm, &Launch<O, D>::ragged_mk, &Launch<O, D>::ragged_mk_warps, &Launch<O, D>::seg_warp, &Launch<O, D>::seg_tma,     \
                             &Launch<O, D>::seg_group, &Launch<O, D>::finalize, &Launch<O, D>::exchange};\
     return &t;                                                                                         \
   }
@@ -1029,6 +1064,73 @@ ipm_status ipm_reduce_ragged(ipm_op op, ipm_dtype dt, const void* dev, const int
     else if (kern == 4) tb->ragged_lpr(p, (int)(nw / IPM_LP_WARPS), nw, st);
 
     else CK(tb->ragged_tile(p, (int)nw, st));
+  }
+  CK(cudaGetLastError());
+  return IPM_OK;
+}
+
+// marked rows: scratch = [bitmap words][chunk counts], each section 256-byte aligned; bounds from the element
+// array's length (positions relative to the chunk origin G >= off[0] - 7 reach at most nvalues + 7)
+static size_t rmk_bits_bytes(int64_t nvalues) { return (((size_t)(nvalues + 64) / 32 + 1) * 4 + 255) & ~(size_t)255; }
+static size_t rmk_cnt_bytes(ipm_dtype dt, int64_t nvalues) {
+  const int64_t ch = 32 * 32 / (int64_t)esize(dt) * 2;  // the marked kernel's smallest chunk (2 vectors per lane)
+  return (((size_t)((nvalues + 64) / ch + 2)) * 4 + 255) & ~(size_t)255;
+}
+size_t ipm_ragged_scratch_bytes(ipm_dtype dt, int64_t nvalues) {
+  if (nvalues < 0 || esize(dt) == 0) return 0;
+  return rmk_bits_bytes(nvalues) + rmk_cnt_bytes(dt, nvalues);
+}
+
+ipm_status ipm_reduce_ragged_marked(ipm_op op, ipm_dtype dt, const void* dev, int64_t nvalues,
+                                    const int64_t* dev_offsets, int64_t rows, const void* init, void* dev_out,
+                                    void* ws, void* scratch, size_t scratch_bytes, void* stream) {
+  ipm_status s;
+  if ((s = validate(op, dt)) || (s = check_ws(ws))) return s;
+  if (rows < 0 || nvalues < 0) {
+    set_error("negative row or element count");
+    return IPM_E_SIZE;
+  }
+  if (rows == 0) return IPM_OK;
+  if (rows >= INT32_MAX) {
+    set_error("ragged: at most 2^31-2 rows");
+    return IPM_E_SIZE;
+  }
+  if (!dev_offsets || !dev_out || !scratch || (!dev && nvalues > 0)) {
+    set_error("NULL device pointer");
+    return IPM_E_NULL;
+  }
+  if (((uintptr_t)dev_out % esize(dt)) || (dev && ((uintptr_t)dev % esize(dt))) || ((uintptr_t)dev_offsets & 7u) ||
+      ((uintptr_t)scratch & 255u)) {
+    set_error("device pointer not aligned to its element size (scratch: 256 bytes)");
+    return IPM_E_ALIGN;
+  }
+  if (scratch_bytes < ipm_ragged_scratch_bytes(dt, nvalues)) {
+    set_error("ragged scratch smaller than ipm_ragged_scratch_bytes(dt, nvalues)");
+    return IPM_E_WORKSPACE;
+  }
+  RaggedParams p;
+  p.a = dev;
+  p.off = dev_offsets;
+  p.rows = rows;
+  p.init = scalar_bits(dt, init);
+  p.has_init = init != nullptr;
+  p.out = dev_out;
+  p.gate = 0;
+  p.gate_len = 0;
+  int64_t* base = (int64_t*)((char*)ws + WS_RAGGED);
+  p.head_row = base;
+  p.head_part = (uint64_t*)(base + WS_MAX_RAGGED_WARPS);
+  p.tail_row = base + 2 * WS_MAX_RAGGED_WARPS;
+  p.tail_part = (uint64_t*)(base + 3 * WS_MAX_RAGGED_WARPS);
+  RaggedMarks m;
+  m.bits = (uint32_t*)scratch;
+  m.cnt = (uint32_t*)((char*)scratch + rmk_bits_bytes(nvalues));
+  const Table* tb = table(op, dt);
+  const int64_t nw = tb->ragged_mk_warps(sm_count());
+  cudaStream_t st = (cudaStream_t)stream;
+  {
+    ProfScope ps(st, 4);
+    CK(tb->ragged_mk(p, m, ipm_ragged_scratch_bytes(dt, nvalues), sm_count(), nw, st));
   }
   CK(cudaGetLastError());
   return IPM_OK;

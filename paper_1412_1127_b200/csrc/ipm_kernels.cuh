@@ -1258,6 +1258,343 @@ __global__ void __launch_bounds__(256) k_ragged_fix(RaggedParams p, int64_t nw) 
   }
 }
 
+// ------------------------------------------------------------------------------------------ ragged, marked rows
+// Two passes (round 2, IPM_OPT_RAGGED_KERNEL = 5 / ipm_reduce_ragged_marked). In k_ragged_vec the
+// per-chunk loop over windows of row offsets (find the rows that start in the chunk, flag their positions, map
+// position -> row) cost ~70 M of 242 M warp instructions on the power-law graph and held the kernel's main stall
+// (profiles/r01_ncu_ragged5_*). Here that work is done once, row-parallel, before the element pass:
+//  pass 0 (k_ragged_mark, one lane per row): bit (off[r] - G) of a bitmap over the elements is set for every row
+//    (G: the first element's index rounded down to a 32-byte address, the origin of the chunk grid), cnt[c] counts
+//    the rows that start in chunk c (CH elements from G; bit 31: one of them is empty), and every EMPTY row is
+//    written here (its result is init ⊕ identity);
+//  pass 1 (k_ragged_mk, element-parallel): warp w owns whole chunks; per chunk each lane reads its EPL flag bits
+//    from the bitmap (one 32-bit load), folds its elements with parking exactly as k_ragged_vec, and names rows by
+//    RANK: the k-th flagged position of the chunk starts row R + k, R = rows started before the chunk (a running
+//    sum of cnt). In a chunk that holds an empty row (cnt bit 31) a flag's row is found by a binary search of the
+//    chunk's rows (the last row starting at or before the flag). Rows crossing warps: head / tail records and
+//    k_ragged_fix as for the other kernels.
+// Scratch (caller-owned, ipm_ragged_scratch_bytes): the bitmap and the chunk counts, zeroed by the launcher.
+struct RaggedMarks {
+  uint32_t* bits;  // bit q = some row starts at element G + q
+  uint32_t* cnt;   // per chunk: rows starting in it (bits 0..30), one of them empty (bit 31)
+};
+
+template <class B>
+__device__ __forceinline__ int64_t ragged_origin(const void* a, int64_t P0) {
+  return P0 - (int64_t)(((uintptr_t)((const B*)a + P0) & 31u) / sizeof(B));
+}
+
+// pass 0: 128 consecutive rows per warp step, 4 per lane (one 32-byte load of off[] per lane, the next step's
+// issued before this one is processed). The row starts' bits are OR-ed into a per-warp shared-memory window of
+// the 64 bitmap words from the step's first row, its row counts into a window of the 8 chunks from the first
+// row's chunk (shared atomics); a row beyond a window (rows longer than 16 elements on average) updates global
+// memory itself. Each non-zero word is then written once: plainly if only this step's rows can start in it
+// (strictly between its first and last row's words), atomically at the two ends (shared with the neighbouring
+// steps); chunk counts are added atomically. Empty rows: result written, chunk flagged (bit 31).
+template <class R, int CH>
+__global__ void __launch_bounds__(256) k_ragged_mark(RaggedParams p, RaggedMarks m) {
+  using B = typename R::B;
+  static_assert((CH & (CH - 1)) == 0, "chunk: a power of two");
+  constexpr int LCH = __builtin_ctz(CH);
+  __shared__ uint32_t s_win[8][64];
+  __shared__ uint32_t s_cnt[8][8];
+  const int lane = threadIdx.x & 31;
+  uint32_t* win = s_win[threadIdx.x >> 5];
+  uint32_t* cwin = s_cnt[threadIdx.x >> 5];
+  win[lane] = 0u;
+  win[lane + 32] = 0u;
+  if (lane < 8) cwin[lane] = 0u;
+  const int64_t rows = p.rows;
+  const int64_t P0 = __ldg(p.off);
+  const int64_t G = ragged_origin<B>(p.a, P0);
+  const B empty_val = R::fin(p.has_init ? R::op(R::lift((B)p.init), R::id()) : R::id());
+  const int64_t stride = (int64_t)gridDim.x * 8 * 128;
+  const bool vec = ((uintptr_t)p.off & 31u) == 0;  // 32-byte loads of 4 offsets
+  // off[b + 4 lane + u], u < 4 (clamped to off[rows])
+  auto load4 = [&](int64_t b, int64_t (&v)[4]) {
+    const int64_t r = b + 4 * lane;
+    if (vec && r + 3 < rows) {
+      const V4 t = ldv<1>((const V4*)(p.off + r));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = (int64_t)t.w[u];
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldg(p.off + (r + u < rows ? r + u : rows));
+    }
+  };
+  int64_t b = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * 128;
+  int64_t nx[4];
+  if (b < rows) load4(b, nx);
+  __syncwarp();
+  for (; b < rows; b += stride) {
+    int64_t sv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) sv[u] = nx[u];
+    const int64_t bend = b + 128 < rows ? b + 128 : rows;
+    const int64_t s_end = __ldg(p.off + bend);  // the end of the step's last row
+    if (b + stride < rows) load4(b + stride, nx);
+    const int64_t q0 = __shfl_sync(FULL, sv[0], 0) - G;  // the step's first row start, relative to G
+    const int64_t w0 = q0 >> 5, c0 = q0 >> LCH;
+    const int64_t nxt = __shfl_down_sync(FULL, sv[0], 1);
+    const int64_t e3 = lane == 31 ? s_end : nxt;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t r = b + 4 * lane + u;
+      if (r < rows) {
+        const int64_t q = sv[u] - G;
+        const int64_t e = u < 3 ? sv[u + 1 < 4 ? u + 1 : 3] : e3;
+        const int64_t dw = (q >> 5) - w0, dc = (q >> LCH) - c0;
+        const uint32_t bit = 1u << (q & 31);
+        if (dw < 64) atomicOr(win + dw, bit);
+        else atomicOr(m.bits + (q >> 5), bit);
+        if (dc < 8) atomicAdd(cwin + dc, 1u);
+        else atomicAdd(m.cnt + (q >> LCH), 1u);
+        if (e == sv[u]) {
+          ((B*)p.out)[r] = empty_val;
+          atomicOr(m.cnt + (q >> LCH), 0x80000000u);
+        }
+      }
+    }
+    // the step's last row's word, relative to w0
+    const int lastl = (int)((bend - 1 - b) >> 2), lastu = (int)((bend - 1 - b) & 3);
+    const int64_t sl = __shfl_sync(FULL, lastu == 0 ? sv[0] : lastu == 1 ? sv[1] : lastu == 2 ? sv[2] : sv[3], lastl);
+    const int64_t dwl = ((sl - G) >> 5) - w0;
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int dw = lane + 32 * h;
+      const uint32_t word = win[dw];
+      win[dw] = 0u;
+      if (word) {
+        if (dw == 0 || dw == dwl) atomicOr(m.bits + w0 + dw, word);
+        else m.bits[w0 + dw] = word;
+      }
+    }
+    if (lane < 8) {
+      const uint32_t c = cwin[lane];
+      cwin[lane] = 0u;
+      if (c) atomicAdd(m.cnt + c0 + lane, c);
+    }
+    __syncwarp();
+  }
+}
+
+template <class R, int WARPS, int MINB, int VPL, int PFD = 0>
+__global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_mk(RaggedParams p, RaggedMarks m) {
+  using B = typename R::B;
+  using A = typename R::A;
+  using VT = typename Vec<B>::T;
+  constexpr int VW = Vec<B>::W;
+  constexpr int EPL = VW * VPL;  // elements per lane per chunk: 16 (4-byte) / 8 (8-byte) flag bits
+  constexpr int CH = 32 * EPL;
+  static_assert(EPL == 32 || EPL == 16 || EPL == 8, "a lane's flags are a 32-, 16- or 8-bit field of one bitmap word");
+  // per warp, column-major by lane: the value of the segment that ends just before a flagged position; and, in a
+  // chunk that holds an empty row, the row of each of the first RMAP flags (by rank)
+  constexpr int RMAP = 64;
+  __shared__ A s_val[WARPS][CH];
+  __shared__ int s_rmap[WARPS][RMAP];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  A* const val_col = s_val[wid] + lane;
+  int* const rmap = s_rmap[wid];
+  const int64_t w = (int64_t)blockIdx.x * WARPS + wid, nw = (int64_t)gridDim.x * WARPS;
+  const B* a = (const B*)p.a;
+  const int64_t P0 = __ldg(p.off), P1 = __ldg(p.off + p.rows);
+  const int64_t G = ragged_origin<B>(p.a, P0);
+  const int64_t NC = P1 > P0 ? (P1 - G + CH - 1) / CH : 0;  // chunks holding elements
+  const int64_t c_lo = (int64_t)(((__int128)NC * w) / nw), c_hi = (int64_t)(((__int128)NC * (w + 1)) / nw);
+  const int64_t lo = max(P0, G + c_lo * CH), hi = min(P1, G + c_hi * CH);
+  if (lane == 0) {
+    p.head_row[w] = lo < hi ? -1 : -2;
+    p.tail_row[w] = -1;
+  }
+  if (lo >= hi) return;  // warp-uniform
+  const int64_t r0 = warp_lower_bound(p.off, p.rows, lo);
+  const int64_t hrow = (r0 > 0 && __ldg(p.off + r0) > lo) ? r0 - 1 : -1;  // off[r0 - 1] < lo
+  const bool has_init = p.has_init;
+  const A ia = has_init ? R::lift((B)p.init) : R::id();
+  auto finish = [&](int64_t row, A v) { ((B*)p.out)[row] = R::fin(has_init ? R::op(ia, v) : v); };
+  const unsigned lanemask_lt = (1u << lane) - 1u;
+  constexpr unsigned FMASK = EPL == 32 ? 0xffffffffu : (1u << EPL) - 1u;
+  int64_t R0 = r0;  // rows that start before the current chunk
+  int64_t open_rid = hrow;
+  A open_val = R::id();
+  // the chunk's row count and this lane's bitmap word, loaded one chunk ahead (their latency was the kernel's
+  // largest stall when loaded in the chunk that uses them)
+  const uint32_t* bits_l = m.bits + (EPL * lane >> 5);
+  uint32_t cw_n = __ldg(m.cnt + c_lo), bw_n = __ldg(bits_l + ((c_lo * CH) >> 5));
+#pragma unroll 1
+  for (int64_t c = c_lo; c < c_hi; ++c) {
+    const uint32_t cw = cw_n, bw = bw_n;
+    // PFD > 0: lane 0 asks L2 for the chunk PFD ahead (no registers or shared memory held)
+    if (PFD > 0 && lane == 0 && c + PFD < c_hi) {
+      const int64_t pb = G + (c + PFD) * CH;
+      const int64_t pe = min(hi, pb + CH);
+      const uint32_t bytes = (uint32_t)((pe - pb) * (int64_t)sizeof(B)) & ~15u;
+      if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a + pb), "r"(bytes) : "memory");
+    }
+    if (c + 1 < c_hi) {
+      cw_n = __ldg(m.cnt + c + 1);
+      bw_n = __ldg(bits_l + (((c + 1) * CH) >> 5));
+    }
+    const int64_t Bc = G + c * CH;
+    const int rlo_c = (int)(lo > Bc ? lo - Bc : 0);
+    const int rhi_c = (int)(hi - Bc < CH ? hi - Bc : CH);
+    const bool interior = rlo_c == 0 && rhi_c == CH;  // warp-uniform
+    const B* pl = a + Bc + EPL * lane;
+    B x[EPL];
+    if (interior) {
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        const VT t = ldv((const VT*)(pl + v * VW));
+#pragma unroll
+        for (int k = 0; k < VW; ++k) x[v * VW + k] = t.w[k];
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < EPL; ++k) {
+        const int rel = EPL * lane + k;
+        x[k] = (rel >= rlo_c && rel < rhi_c) ? lds(pl + k) : (B)0;
+      }
+    }
+    unsigned fl = (bw >> ((EPL * lane) & 31)) & FMASK;
+    if (!interior) {  // flags of positions outside [lo, hi) (before P0, at or after P1 / the next warp's chunks)
+      const int b0 = rlo_c - EPL * lane, b1 = rhi_c - EPL * lane;
+      const unsigned keep_lo = b0 <= 0 ? FMASK : b0 >= EPL ? 0u : (FMASK & ~((1u << b0) - 1u));
+      const unsigned keep_hi = b1 >= EPL ? FMASK : b1 <= 0 ? 0u : ((1u << b1) - 1u);
+      fl &= keep_lo & keep_hi;
+    }
+    const unsigned bal = __ballot_sync(FULL, fl != 0u);
+    if (bal == 0u) {  // no row starts in the chunk: every element continues open_rid
+      A v = R::id();
+      if (interior) {
+#pragma unroll
+        for (int k = 0; k < EPL; ++k) v = R::op(v, R::lift(x[k]));
+      } else {
+#pragma unroll
+        for (int k = 0; k < EPL; ++k) {
+          const int rel = EPL * lane + k;
+          v = R::op(v, (rel >= rlo_c && rel < rhi_c) ? R::lift(x[k]) : R::id());
+        }
+      }
+      open_val = R::op(open_val, R::warp(v));
+      R0 += cw & 0x7fffffffu;
+      continue;
+    }
+    // lane-local segmented fold, one pass, parking at every flag (as k_ragged_vec)
+    A acc = R::id();
+    if (interior) {
+#pragma unroll
+      for (int k = 0; k < EPL; ++k) {
+        const bool s = (fl >> k) & 1u;
+        if (s) val_col[k * 32] = acc;
+        acc = R::op(s ? R::id() : acc, R::lift(x[k]));
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < EPL; ++k) {
+        const int rel = EPL * lane + k;
+        const bool s = (fl >> k) & 1u;
+        if (s) val_col[k * 32] = acc;
+        acc = R::op(s ? R::id() : acc, (rel >= rlo_c && rel < rhi_c) ? R::lift(x[k]) : R::id());
+      }
+    }
+    // rank of the lane's first flag in the chunk: exclusive prefix of the flag counts
+    const int nf = __popc(fl);
+    int pre = nf;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int o = __shfl_up_sync(FULL, pre, d);
+      if (lane >= d) pre += o;
+    }
+    pre -= nf;
+    const bool has_empty = (cw >> 31) != 0u;  // warp-uniform
+    const int64_t cnt_c = cw & 0x7fffffffu;
+    if (has_empty) {  // rank -> row of the chunk's non-empty rows, for the first RMAP ranks (one pass over them)
+      int base = 0;
+      for (int64_t j0 = 0; j0 < cnt_c && base < RMAP; j0 += 32) {
+        const int64_t j = j0 + lane;
+        const bool in = j < cnt_c;
+        const int64_t st = in ? __ldg(p.off + R0 + j) : 0, en = in ? __ldg(p.off + R0 + j + 1) : 0;
+        const unsigned ne = __ballot_sync(FULL, in && en > st);
+        const int rk = base + __popc(ne & lanemask_lt);
+        if (((ne >> lane) & 1u) && rk < RMAP) rmap[rk] = (int)(j);
+        base += __popc(ne);
+      }
+      __syncwarp();
+    }
+    // the row that starts at the lane's flag k (k-th bit): by rank, or (a chunk with an empty row) from the map,
+    // beyond it the last of the chunk's rows that starts at or before the position
+    auto rid_of = [&](int k, int rank) -> int64_t {
+      if (!has_empty) return R0 + rank;
+      if (rank < RMAP) return R0 + rmap[rank];
+      const int64_t pos = Bc + EPL * lane + k;
+      int64_t l = R0, h = R0 + cnt_c - 1;
+      while (l < h) {
+        const int64_t mid = (l + h + 1) >> 1;
+        if (__ldg(p.off + mid) <= pos) l = mid;
+        else h = mid - 1;
+      }
+      return l;
+    };
+    const int kf = fl ? __ffs(fl) - 1 : EPL;
+    const int kl = fl ? 31 - __clz(fl) : EPL;
+    const A head = fl ? val_col[kf * 32] : acc;
+    const A cur = fl ? acc : R::id();
+    {  // rows that start and end inside this lane: between consecutive flags, value parked at the later one
+      int rank = pre;
+      for (unsigned mm = fl & ~(1u << kl); mm; mm &= mm - 1, ++rank) {
+        const int k0 = __ffs(mm) - 1;
+        const int k1 = __ffs(fl & ~((2u << k0) - 1u)) - 1;
+        finish(rid_of(k0, rank), val_col[k1 * 32]);
+      }
+    }
+    const bool flag = fl != 0u;
+    const long long my_rid = flag ? (long long)rid_of(kl, pre + nf - 1) : -1;
+    // segmented inclusive scan over lanes: a flagged lane starts a segment with its tail value
+    const unsigned le = bal & (lanemask_lt | (1u << lane));
+    const int start = le ? 31 - __clz(le) : 0;
+    A sv = flag ? cur : head;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const A ov = shfl_up_acc(sv, d);
+      if (lane - d >= start) sv = R::op(ov, sv);
+    }
+    // the row open at this lane's start
+    const unsigned lt = bal & lanemask_lt;
+    A ev = shfl_up_acc(sv, 1);
+    const int src = lt ? 31 - __clz(lt) : 0;
+    const long long rr = __shfl_sync(FULL, my_rid, src);
+    if (!lt) ev = lane == 0 ? open_val : R::op(open_val, ev);
+    const long long er = lt ? rr : open_rid;
+    if (flag && er >= 0) {  // it ends at this lane's first flag
+      const A v = R::op(ev, head);
+      if (er == hrow) {
+        p.head_row[w] = hrow;
+        p.head_part[w] = pack(v);
+      } else {
+        finish(er, v);
+      }
+    }
+    // carry into the next chunk: the row open at the end of lane 31
+    open_val = shfl_acc(sv, 31);
+    open_rid = __shfl_sync(FULL, my_rid, 31 - __clz(bal));
+    R0 += cnt_c;
+    __syncwarp();
+  }
+  // the row still open at hi
+  if (lane == 0 && open_rid >= 0) {
+    if (open_rid == hrow) {
+      p.head_row[w] = hrow;
+      p.head_part[w] = pack(open_val);
+    } else if (__ldg(p.off + open_rid + 1) <= hi) {
+      finish(open_rid, open_val);
+    } else {
+      p.tail_row[w] = open_rid;
+      p.tail_part[w] = pack(open_val);
+    }
+  }
+}
+
 
 // ------------------------------------------------------------------------------------------ ragged, row order
 // k_ragged_rank: the ownership rules, chunk shape and lane fold of k_ragged_vec, with the per-chunk row bookkeeping

@@ -60,6 +60,8 @@ def _load():
         "ipm_reduce_async": ([ci, ci, vp, i64, vp, vp, vp, vp], ci),
         "ipm_reduce_segmented": ([ci, ci, vp, i64, i64, i64, vp, vp, vp, vp], ci),
         "ipm_reduce_ragged": ([ci, ci, vp, vp, i64, vp, vp, vp, vp], ci),
+        "ipm_ragged_scratch_bytes": ([ci, i64], sz),
+        "ipm_reduce_ragged_marked": ([ci, ci, vp, i64, vp, i64, vp, vp, vp, vp, sz, vp], ci),
         "ipm_reduce_partials": ([ci, ci, vp, i64, vp, ci, ctypes.POINTER(ci), vp], ci),
         "ipm_finalize_partials": ([ci, ci, vp, ci, vp, vp, vp], ci),
         "ipm_reduce_2d": ([ci, ci, vp, i64, i64, i64, vp, vp, vp], ci),
@@ -104,7 +106,7 @@ lib = _load()
 EXPORTED = ("ipm_status_str ipm_last_error_message ipm_op_legal ipm_dtype_size ipm_version ipm_set_allocator "
             "ipm_copyin ipm_create ipm_present ipm_update_device ipm_update_host ipm_copyout ipm_delete "
             "ipm_present_count ipm_workspace_bytes ipm_workspace_init ipm_reduce ipm_reduce_async "
-            "ipm_reduce_segmented ipm_reduce_ragged ipm_reduce_partials ipm_finalize_partials ipm_reduce_2d ipm_reduce_2d_async ipm_fused_nvars ipm_reduce_fused ipm_reduce_fused_async ipm_reduce_host ipm_release_staging ipm_set_option ipm_profile_enable ipm_profile_read "
+            "ipm_reduce_segmented ipm_reduce_ragged ipm_ragged_scratch_bytes ipm_reduce_ragged_marked ipm_reduce_partials ipm_finalize_partials ipm_reduce_2d ipm_reduce_2d_async ipm_fused_nvars ipm_reduce_fused ipm_reduce_fused_async ipm_reduce_host ipm_release_staging ipm_set_option ipm_profile_enable ipm_profile_read "
             "ipm_profile_disable ipm_flat_geometry ipm_flat_schedule ipm_identity ipm_comm_id_bytes "
             "ipm_comm_unique_id ipm_comm_init ipm_comm_destroy ipm_comm_init_group ipm_comm_ipc_handle_bytes "
             "ipm_comm_create_ipc ipm_comm_attach_ipc ipm_shard_range ipm_comm_uses_peer_memory ipm_comm_error "
@@ -318,6 +320,14 @@ def reduce_ragged(op: str, values: torch.Tensor, offsets: torch.Tensor, init=Non
         _check_out(out, values, rows)
     ws = workspace(stream) if ws is None else ws
     box = _scalar(dt, init)
+    if _ragged_marked[0]:  # two passes over scratch from torch's caching allocator (ipm_reduce_ragged_marked)
+        nvalues = values.numel()
+        scratch = torch.empty(lib.ipm_ragged_scratch_bytes(dt, nvalues), dtype=torch.uint8, device=values.device)
+        _check(lib.ipm_reduce_ragged_marked(op_code(op), dt, ptr, nvalues, offsets.data_ptr(), rows,
+                                            None if box is None else box.ctypes.data, out.data_ptr(), ws.data_ptr(),
+                                            scratch.data_ptr(), scratch.numel(), _stream(stream)),
+               "ipm_reduce_ragged_marked")
+        return out
     _check(lib.ipm_reduce_ragged(op_code(op), dt, ptr, offsets.data_ptr(), rows,
                                  None if box is None else box.ctypes.data, out.data_ptr(), ws.data_ptr(),
                                  _stream(stream)), "ipm_reduce_ragged")
@@ -460,6 +470,8 @@ def identity_value(op: str, dt: int):
 OPTIONS = {"flat_ctas_per_sm": 0, "seg_kernel": 1, "deterministic": 2, "dist_mode": 3, "dist_timeout_ms": 4,
            "ragged_kernel": 5}
 RAGGED_KERNELS = {"auto": 0, "warp": 1, "tile": 2, "rank": 3, "lpr": 4}
+# "marked": reduce_ragged calls ipm_reduce_ragged_marked (two passes over scratch) instead of ipm_reduce_ragged
+_ragged_marked = [False]
 DIST_MODES = {"auto": 0, "p2p": 0, "nccl": 1}
 SEG_KERNELS = {"auto": 0, "warp": 1, "ldg": 1, "tma": 2}
 
@@ -472,7 +484,8 @@ def set_option(key: str, value) -> None:
     if key == "dist_mode" and isinstance(value, str):
         value = DIST_MODES[value]
     if key == "ragged_kernel" and isinstance(value, str):
-        value = RAGGED_KERNELS[value]
+        _ragged_marked[0] = value == "marked"
+        value = RAGGED_KERNELS.get(value, 0)
     _check(lib.ipm_set_option(OPTIONS[key], int(value)), "ipm_set_option")
 
 

@@ -80,6 +80,18 @@ def test_validation_before_cuda(ipm):
     assert L.ipm_reduce_segmented(5, 3, dev, 5, 10, 10, None, out, ws, None) == 1  # | on float64
     assert L.ipm_reduce_host(0, 0, None, 10, box, ws, None) == 3
     assert "illegal" in L.ipm_last_error_message().decode() or L.ipm_last_error_message()
+    # marked ragged rows: scratch size from the element count (bitmap bit per element + a count per chunk)
+    offs, scr = ctypes.c_void_p(0x40000), ctypes.c_void_p(0x50000)
+    need = L.ipm_ragged_scratch_bytes(2, 1 << 20)
+    assert (1 << 20) // 8 < need <= (1 << 20) // 8 + (1 << 20) // 256 * 4 + 1024
+    assert need % 256 == 0 and L.ipm_ragged_scratch_bytes(3, 1 << 20) > need  # 8-byte types: half-size chunks
+    assert L.ipm_reduce_ragged_marked(0, 2, dev, 1 << 20, offs, 100, None, out, ws, scr, need - 256, None) == 7
+    assert L.ipm_reduce_ragged_marked(0, 2, dev, 1 << 20, offs, 100, None, out, ws, ctypes.c_void_p(0x50010),
+                                      need, None) == 6                        # scratch alignment
+    assert L.ipm_reduce_ragged_marked(4, 2, dev, 1 << 20, offs, 100, None, out, ws, scr, need, None) == 1
+    assert L.ipm_reduce_ragged_marked(0, 2, dev, 1 << 20, None, 100, None, out, ws, scr, need, None) == 3
+    assert L.ipm_reduce_ragged_marked(0, 2, dev, -1, offs, 100, None, out, ws, scr, need, None) == 4
+    assert L.ipm_reduce_ragged_marked(0, 2, dev, 1 << 20, offs, 0, None, out, ws, scr, need, None) == 0  # no rows
 
 
 def test_present_table_errors(ipm):

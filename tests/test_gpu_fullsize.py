@@ -132,7 +132,7 @@ def _ragged_graph(kind):
     return ipmgen.offsets_from_degrees(ipmgen.degrees(1 << 16, seed=1, kind="const", mean=4096.0))
 
 
-@pytest.mark.parametrize("kern", ["auto", "warp", "rank", "lpr"])
+@pytest.mark.parametrize("kern", ["auto", "warp", "rank", "lpr", "marked"])
 @pytest.mark.parametrize("kind", ["powerlaw", "const4096"])
 def test_ragged_fullsize(ipm, kind, kern):
     off = _ragged_graph(kind)

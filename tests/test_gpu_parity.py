@@ -420,7 +420,7 @@ def ragged_cases():
     yield "empties_and_giant", ipmgen.offsets_from_degrees(d, 7)
 
 
-@pytest.fixture(params=["auto", "tile", "warp", "rank", "lpr"])
+@pytest.fixture(params=["auto", "tile", "warp", "rank", "lpr", "marked"])
 def ragged_kernel(request, ipm):
     ipm.set_option("ragged_kernel", request.param)
     yield request.param

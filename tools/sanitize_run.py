@@ -37,7 +37,7 @@ print("sanitize_run: ok")
 
 
 def ragged_all(op, x, off):
-    for kern in ("auto", "warp", "tile", "rank", "lpr"):
+    for kern in ("auto", "warp", "tile", "rank", "lpr", "marked"):
         ipm.set_option("ragged_kernel", kern)
         ipm.reduce_ragged(op, x, off)
     ipm.set_option("ragged_kernel", "auto")
