@@ -349,6 +349,16 @@ def suite(ipm, torch, ipmgen, peak):
                                                "kernels_per_call": 3,
                                                "kernels_note": "k_ragged_vec (runs: mean row length 16 < 256), "
                                                                "k_ragged_lpr (returns after its gate), k_ragged_fix"}
+    # the same graph through the two-pass path (ipm_reduce_ragged_marked, scratch from torch's allocator)
+    ipm.set_option("ragged_kernel", "marked")
+    try:
+        ms = timed(lambda: ipm.reduce_ragged("+", vals, offs, out=o, ws=ws))
+    finally:
+        ipm.set_option("ragged_kernel", "auto")
+    med = statistics.median(ms)
+    out["ragged_float32_powerlaw_2^24rows_marked"] = {
+        "ms_median": med, "GB/s": nbytes / med / 1e6, "frac": nbytes / med / 1e6 / peak, "kernel": "marked",
+        "kernels_per_call": 4, "kernels_note": "memset of the scratch, k_ragged_mark, k_ragged_mk, k_ragged_fix"}
     del vals, offs, o
     torch.cuda.empty_cache()
     # library context: CUB's DeviceReduce / DeviceSegmentedReduce on the same shapes, including this ragged graph

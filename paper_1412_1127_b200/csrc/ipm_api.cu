@@ -1125,6 +1125,8 @@ ipm_status ipm_reduce_ragged_marked(ipm_op op, ipm_dtype dt, const void* dev, in
   RaggedMarks m;
   m.bits = (uint32_t*)scratch;
   m.cnt = (uint32_t*)((char*)scratch + rmk_bits_bytes(nvalues));
+  m.nwords = (int64_t)(rmk_bits_bytes(nvalues) / 4);
+  m.nchunks = (int64_t)(rmk_cnt_bytes(dt, nvalues) / 4);
   const Table* tb = table(op, dt);
   const int64_t nw = tb->ragged_mk_warps(sm_count());
   cudaStream_t st = (cudaStream_t)stream;

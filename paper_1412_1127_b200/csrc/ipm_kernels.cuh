@@ -1277,7 +1277,20 @@ __global__ void __launch_bounds__(256) k_ragged_fix(RaggedParams p, int64_t nw) 
 struct RaggedMarks {
   uint32_t* bits;  // bit q = some row starts at element G + q
   uint32_t* cnt;   // per chunk: rows starting in it (bits 0..30), one of them empty (bit 31)
+  int64_t nwords, nchunks;  // their sizes (checked in the IPM_CHECK_BOUNDS build)
 };
+// IPM_CHECK_BOUNDS (a test build, tools/gpu_bounds.sh; compute-sanitizer is not available on the GPU pool): every
+// scratch, output and offsets index of the marked kernels is checked and a violation traps
+#ifdef IPM_CHECK_BOUNDS
+#define IPM_BOUND(c) \
+  do {               \
+    if (!(c)) __trap(); \
+  } while (0)
+#else
+#define IPM_BOUND(c) \
+  do {               \
+  } while (0)
+#endif
 
 template <class B>
 __device__ __forceinline__ int64_t ragged_origin(const void* a, int64_t P0) {
@@ -1345,6 +1358,7 @@ __global__ void __launch_bounds__(256) k_ragged_mark(RaggedParams p, RaggedMarks
         const int64_t e = u < 3 ? sv[u + 1 < 4 ? u + 1 : 3] : e3;
         const int64_t dw = (q >> 5) - w0, dc = (q >> LCH) - c0;
         const uint32_t bit = 1u << (q & 31);
+        IPM_BOUND(q >= 0 && (q >> 5) < m.nwords && (q >> LCH) < m.nchunks && dw >= 0 && dc >= 0);
         if (dw < 64) atomicOr(win + dw, bit);
         else atomicOr(m.bits + (q >> 5), bit);
         if (dc < 8) atomicAdd(cwin + dc, 1u);
@@ -1366,6 +1380,7 @@ __global__ void __launch_bounds__(256) k_ragged_mark(RaggedParams p, RaggedMarks
       const uint32_t word = win[dw];
       win[dw] = 0u;
       if (word) {
+        IPM_BOUND(w0 + dw < m.nwords);
         if (dw == 0 || dw == dwl) atomicOr(m.bits + w0 + dw, word);
         else m.bits[w0 + dw] = word;
       }
@@ -1373,7 +1388,10 @@ __global__ void __launch_bounds__(256) k_ragged_mark(RaggedParams p, RaggedMarks
     if (lane < 8) {
       const uint32_t c = cwin[lane];
       cwin[lane] = 0u;
-      if (c) atomicAdd(m.cnt + c0 + lane, c);
+      if (c) {
+        IPM_BOUND(c0 + lane < m.nchunks);
+        atomicAdd(m.cnt + c0 + lane, c);
+      }
     }
     __syncwarp();
   }
@@ -1412,7 +1430,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_mk(RaggedParams p, 
   const int64_t hrow = (r0 > 0 && __ldg(p.off + r0) > lo) ? r0 - 1 : -1;  // off[r0 - 1] < lo
   const bool has_init = p.has_init;
   const A ia = has_init ? R::lift((B)p.init) : R::id();
-  auto finish = [&](int64_t row, A v) { ((B*)p.out)[row] = R::fin(has_init ? R::op(ia, v) : v); };
+  auto finish = [&](int64_t row, A v) {
+    IPM_BOUND(row >= 0 && row < p.rows);
+    ((B*)p.out)[row] = R::fin(has_init ? R::op(ia, v) : v);
+  };
   const unsigned lanemask_lt = (1u << lane) - 1u;
   constexpr unsigned FMASK = EPL == 32 ? 0xffffffffu : (1u << EPL) - 1u;
   int64_t R0 = r0;  // rows that start before the current chunk
@@ -1421,6 +1442,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_mk(RaggedParams p, 
   // the chunk's row count and this lane's bitmap word, loaded one chunk ahead (their latency was the kernel's
   // largest stall when loaded in the chunk that uses them)
   const uint32_t* bits_l = m.bits + (EPL * lane >> 5);
+  IPM_BOUND(c_hi <= m.nchunks && (((c_hi - 1) * CH) >> 5) + 1 <= m.nwords && r0 <= p.rows);
   uint32_t cw_n = __ldg(m.cnt + c_lo), bw_n = __ldg(bits_l + ((c_lo * CH) >> 5));
 #pragma unroll 1
   for (int64_t c = c_lo; c < c_hi; ++c) {
@@ -1440,6 +1462,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_mk(RaggedParams p, 
     const int rlo_c = (int)(lo > Bc ? lo - Bc : 0);
     const int rhi_c = (int)(hi - Bc < CH ? hi - Bc : CH);
     const bool interior = rlo_c == 0 && rhi_c == CH;  // warp-uniform
+    IPM_BOUND(!interior || (Bc >= lo && Bc + CH <= hi));
     const B* pl = a + Bc + EPL * lane;
     B x[EPL];
     if (interior) {
@@ -1498,7 +1521,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_mk(RaggedParams p, 
         acc = R::op(s ? R::id() : acc, (rel >= rlo_c && rel < rhi_c) ? R::lift(x[k]) : R::id());
       }
     }
-    // rank of the lane's first flag in the chunk: exclusive prefix of the flag counts
+    // rank of the lane's first flag in the chunk: exclusive prefix of the flag counts (a per-bit ballot form
+    // measured 1-4 % slower, profiles/r02_ab_marked_2.txt)
     const int nf = __popc(fl);
     int pre = nf;
 #pragma unroll
@@ -1517,6 +1541,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_mk(RaggedParams p, 
         const int64_t st = in ? __ldg(p.off + R0 + j) : 0, en = in ? __ldg(p.off + R0 + j + 1) : 0;
         const unsigned ne = __ballot_sync(FULL, in && en > st);
         const int rk = base + __popc(ne & lanemask_lt);
+        IPM_BOUND(!in || R0 + j + 1 <= p.rows);
         if (((ne >> lane) & 1u) && rk < RMAP) rmap[rk] = (int)(j);
         base += __popc(ne);
       }
