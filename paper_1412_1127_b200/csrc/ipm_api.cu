@@ -334,7 +334,7 @@ struct Launch {
                                cudaStream_t st) {
     cudaError_t e = cudaMemsetAsync(m.bits, 0, zero_bytes, st);
     if (e != cudaSuccess) return e;
-    const int64_t blocks0 = std::min<int64_t>((p.rows + 1023) / 1024, (int64_t)sms * 8);  // 8 warps x 128 rows
+    const int64_t blocks0 = std::min<int64_t>((p.rows + 1023) / 1024, (int64_t)sms * 4);  // 8 warps x 128 rows; 4 CTAs per SM fit (58 registers)
     k_ragged_mark<R, MK_CH><<<(unsigned)blocks0, 256, 0, st>>>(p, m);
     static const bool carveout = cudaFuncSetAttribute(k_ragged_mk<R, 4, MK_MINB, MK_VPL, MK_PFD>,
                                                       cudaFuncAttributePreferredSharedMemoryCarveout,

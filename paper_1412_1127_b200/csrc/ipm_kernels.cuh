@@ -1258,6 +1258,13 @@ __global__ void __launch_bounds__(256) k_ragged_fix(RaggedParams p, int64_t nw) 
   }
 }
 
+__device__ __forceinline__ void cp_async8(void* s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(s)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 // ------------------------------------------------------------------------------------------ ragged, marked rows
 // Two passes (round 2, IPM_OPT_RAGGED_KERNEL = 5 / ipm_reduce_ragged_marked). In k_ragged_vec the
 // per-chunk loop over windows of row offsets (find the rows that start in the chunk, flag their positions, map
@@ -1336,20 +1343,49 @@ __global__ void __launch_bounds__(256) k_ragged_mark(RaggedParams p, RaggedMarks
     }
   };
   int64_t b = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * 128;
-  int64_t nx[4];
-  if (b < rows) load4(b, nx);
+  int64_t nx[4], nx_end = 0;  // the next step's offsets and the end of its last row, loaded a step ahead
+  if (b < rows) {
+    load4(b, nx);
+    nx_end = __ldg(p.off + (b + 128 < rows ? b + 128 : rows));
+  }
   __syncwarp();
   for (; b < rows; b += stride) {
     int64_t sv[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) sv[u] = nx[u];
     const int64_t bend = b + 128 < rows ? b + 128 : rows;
-    const int64_t s_end = __ldg(p.off + bend);  // the end of the step's last row
-    if (b + stride < rows) load4(b + stride, nx);
+    const int64_t s_end = nx_end;  // the end of the step's last row
+    if (b + stride < rows) {
+      load4(b + stride, nx);
+      nx_end = __ldg(p.off + (b + stride + 128 < rows ? b + stride + 128 : rows));
+    }
     const int64_t q0 = __shfl_sync(FULL, sv[0], 0) - G;  // the step's first row start, relative to G
     const int64_t w0 = q0 >> 5, c0 = q0 >> LCH;
     const int64_t nxt = __shfl_down_sync(FULL, sv[0], 1);
     const int64_t e3 = lane == 31 ? s_end : nxt;
+    const int nr = (int)(bend - b);                    // rows in this step (<= 128)
+    const int64_t base = G + (w0 << 5);                // bit 0 of the window's first word
+    if (s_end - base < ((int64_t)1 << 31)) {           // warp-uniform: the step spans < 2^31 elements: 32 bits
+      const uint32_t offc = (uint32_t)((w0 << 5) - (c0 << LCH));
+      const uint32_t blo = (uint32_t)base;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (4 * lane + u < nr) {
+          const uint32_t t = (uint32_t)sv[u] - blo;  // position relative to the window's first word
+          const uint32_t e = u < 3 ? (uint32_t)sv[u + 1 < 4 ? u + 1 : 3] : (uint32_t)e3;
+          const uint32_t dw = t >> 5, dc = (t + offc) >> LCH;
+          IPM_BOUND(w0 + dw < m.nwords && c0 + dc < m.nchunks);
+          if (dw < 64) atomicOr(win + dw, 1u << (t & 31));
+          else atomicOr(m.bits + w0 + dw, 1u << (t & 31));
+          if (dc < 8) atomicAdd(cwin + dc, 1u);
+          else atomicAdd(m.cnt + c0 + dc, 1u);
+          if (e == (uint32_t)sv[u]) {
+            ((B*)p.out)[b + 4 * lane + u] = empty_val;
+            atomicOr(m.cnt + c0 + dc, 0x80000000u);
+          }
+        }
+      }
+    } else {
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int64_t r = b + 4 * lane + u;
@@ -1368,6 +1404,7 @@ __global__ void __launch_bounds__(256) k_ragged_mark(RaggedParams p, RaggedMarks
           atomicOr(m.cnt + (q >> LCH), 0x80000000u);
         }
       }
+    }
     }
     // the step's last row's word, relative to w0
     const int lastl = (int)((bend - 1 - b) >> 2), lastu = (int)((bend - 1 - b) & 3);
@@ -1411,9 +1448,12 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_mk(RaggedParams p, 
   constexpr int RMAP = 64;
   __shared__ A s_val[WARPS][CH];
   __shared__ int s_rmap[WARPS][RMAP];
+  __shared__ int64_t s_offn[WARPS][RMAP + 1];  // the next chunk's first RMAP + 1 offsets (cp.async, if it has empties)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   A* const val_col = s_val[wid] + lane;
   int* const rmap = s_rmap[wid];
+  int64_t* const offn = s_offn[wid];
+  bool pf_ready = false;  // warp-uniform: offn holds the current chunk's offsets
   const int64_t w = (int64_t)blockIdx.x * WARPS + wid, nw = (int64_t)gridDim.x * WARPS;
   const B* a = (const B*)p.a;
   const int64_t P0 = __ldg(p.off), P1 = __ldg(p.off + p.rows);
@@ -1433,6 +1473,16 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_mk(RaggedParams p, 
   auto finish = [&](int64_t row, A v) {
     IPM_BOUND(row >= 0 && row < p.rows);
     ((B*)p.out)[row] = R::fin(has_init ? R::op(ia, v) : v);
+  };
+  // copy off[R0n .. R0n + min(cnt, RMAP)] of chunk c + 1 into offn if that chunk holds an empty row
+  auto prefetch_offsets = [&](int64_t c, int64_t R0n, uint32_t cwn) -> bool {
+    if (c + 1 >= c_hi || !(cwn >> 31)) return false;
+    const int64_t lim = min((int64_t)(cwn & 0x7fffffffu), (int64_t)RMAP);
+#pragma unroll
+    for (int i = lane; i <= RMAP; i += 32)
+      if (i <= lim && R0n + i <= p.rows) cp_async8(offn + i, p.off + R0n + i);
+    cp_async_commit();
+    return true;
   };
   const unsigned lanemask_lt = (1u << lane) - 1u;
   constexpr unsigned FMASK = EPL == 32 ? 0xffffffffu : (1u << EPL) - 1u;
@@ -1500,6 +1550,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_mk(RaggedParams p, 
         }
       }
       open_val = R::op(open_val, R::warp(v));
+      if (pf_ready) cp_async_wait<0>();  // (unused: no flags) nothing may land after the buffer is reused
+      pf_ready = prefetch_offsets(c, R0 + (cw & 0x7fffffffu), cw_n);
       R0 += cw & 0x7fffffffu;
       continue;
     }
@@ -1534,11 +1586,17 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_mk(RaggedParams p, 
     const bool has_empty = (cw >> 31) != 0u;  // warp-uniform
     const int64_t cnt_c = cw & 0x7fffffffu;
     if (has_empty) {  // rank -> row of the chunk's non-empty rows, for the first RMAP ranks (one pass over them)
+      if (pf_ready) {
+        cp_async_wait<0>();
+        __syncwarp();
+      }
       int base = 0;
       for (int64_t j0 = 0; j0 < cnt_c && base < RMAP; j0 += 32) {
         const int64_t j = j0 + lane;
         const bool in = j < cnt_c;
-        const int64_t st = in ? __ldg(p.off + R0 + j) : 0, en = in ? __ldg(p.off + R0 + j + 1) : 0;
+        const bool sm = pf_ready && j < RMAP;  // warp-uniform per window (RMAP is a multiple of 32)
+        const int64_t st = !in ? 0 : sm ? offn[j] : __ldg(p.off + R0 + j);
+        const int64_t en = !in ? 0 : sm ? offn[j + 1] : __ldg(p.off + R0 + j + 1);
         const unsigned ne = __ballot_sync(FULL, in && en > st);
         const int rk = base + __popc(ne & lanemask_lt);
         IPM_BOUND(!in || R0 + j + 1 <= p.rows);
@@ -1546,7 +1604,13 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_mk(RaggedParams p, 
         base += __popc(ne);
       }
       __syncwarp();
+    } else if (pf_ready) {
+      cp_async_wait<0>();
+      __syncwarp();
     }
+    // the next chunk's offsets, if it holds an empty row (its count word arrived a chunk ago): copied now, read
+    // when that chunk builds its rank map
+    pf_ready = prefetch_offsets(c, R0 + cnt_c, cw_n);
     // the row that starts at the lane's flag k (k-th bit): by rank, or (a chunk with an empty row) from the map,
     // beyond it the last of the chunk's rows that starts at or before the position
     auto rid_of = [&](int k, int rank) -> int64_t {
@@ -1638,12 +1702,6 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_mk(RaggedParams p, 
 //    before it; then each owning lane reads its row's value at the row's END position (where the next row
 //    starts) and stores out[row]: consecutive rows from consecutive lanes, no per-lane loop, no row map.
 //  Positions are kept relative to the chunk and rows relative to r0 in 32 bits.
-__device__ __forceinline__ void cp_async8(void* s, const void* g) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(s)), "l"(g) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 template <class R, int WARPS, int MINB, int VPL, int NR, int PFV = 0>
 __global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_rank(RaggedParams p) {
