@@ -193,9 +193,10 @@ ipm_status ipm_reduce_fused_async(ipm_fused f, ipm_dtype dt, const void* x, cons
 ipm_status ipm_reduce_ragged(ipm_op op, ipm_dtype dt, const void* dev, const int64_t* dev_offsets, int64_t rows,
                              const void* init, void* dev_out, void* workspace, void* stream);
 
-/* The same clause (identical results, bit for bit on every (op, dtype): the fold of each row is split at the
- * same element positions as in ipm_reduce_ragged's default kernel), computed in two passes over caller-owned
- * scratch: a row-parallel pass marks where every row starts in a bitmap over the elements, counts the row starts
+/* The same clause and the same parity bar as ipm_reduce_ragged (bit-exact for integer, bitwise, logical, max and
+ * min; float + * within the stated tolerance — rows are split into lane and chunk pieces at other positions, so the
+ * float64 association order, and in rare cases the last bit of a float32 row sum, can differ from the default
+ * kernel's; deterministic from run to run), computed in two passes over caller-owned scratch: a row-parallel pass marks where every row starts in a bitmap over the elements, counts the row starts
  * per chunk of 512 elements (256 for 8-byte types) and writes every EMPTY row (init ⊕ identity); an
  * element-parallel pass then folds the elements, reading each lane's row-start flags from the bitmap and naming
  * rows by rank within their chunk instead of walking the row offsets per chunk.
