@@ -323,10 +323,16 @@ def reduce_ragged(op: str, values: torch.Tensor, offsets: torch.Tensor, init=Non
     if _ragged_marked[0]:  # two passes over scratch from torch's caching allocator (ipm_reduce_ragged_marked)
         nvalues = values.numel()
         scratch = torch.empty(lib.ipm_ragged_scratch_bytes(dt, nvalues), dtype=torch.uint8, device=values.device)
+        s = _stream(stream)
         _check(lib.ipm_reduce_ragged_marked(op_code(op), dt, ptr, nvalues, offsets.data_ptr(), rows,
                                             None if box is None else box.ctypes.data, out.data_ptr(), ws.data_ptr(),
-                                            scratch.data_ptr(), scratch.numel(), _stream(stream)),
+                                            scratch.data_ptr(), scratch.numel(), s),
                "ipm_reduce_ragged_marked")
+        if stream is not None:
+            # the scratch was allocated on torch's current stream; the kernels run on `stream`: keep the block out
+            # of the caching allocator's pool until that stream's work so far has completed
+            scratch.record_stream(stream if isinstance(stream, torch.cuda.Stream)
+                                  else torch.cuda.ExternalStream(s, device=values.device))
         return out
     _check(lib.ipm_reduce_ragged(op_code(op), dt, ptr, offsets.data_ptr(), rows,
                                  None if box is None else box.ctypes.data, out.data_ptr(), ws.data_ptr(),

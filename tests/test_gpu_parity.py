@@ -457,6 +457,33 @@ def test_ragged_big_powerlaw_deterministic(ipm, ragged_kernel):
     assert np.array_equal(a, want.astype(np.float32))
 
 
+def test_ragged_marked_side_stream(ipm):
+    """The two-pass path on a caller stream other than torch's current one: its scratch (from torch's caching
+    allocator, allocated on the current stream) must not be handed out again while the kernels still use it —
+    allocations and writes on the current stream right after each call, result checked against the oracle."""
+    off = ipmgen.offsets_from_degrees(ipmgen.degrees(1 << 18, seed=11))
+    spec = ipmgen.Spec("int32", int(off[-1]), "random", seed=11)
+    x = device_input(spec)
+    offs = torch.from_numpy(off).cuda()
+    want, _ = oracle.reduce_ragged("^", ipmgen.fill_host(spec), off)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    ipm.set_option("ragged_kernel", "marked")
+    try:
+        outs = []
+        for _ in range(4):
+            o = torch.empty(off.size - 1, dtype=torch.int32, device="cuda")
+            o.record_stream(side)
+            outs.append(ipm.reduce_ragged("^", x, offs, out=o, stream=side))
+            junk = torch.empty(ipm.lib.ipm_ragged_scratch_bytes(0, x.numel()), dtype=torch.uint8, device="cuda")
+            junk.fill_(0xFF)  # on the current stream, while the side stream may still be running
+        side.synchronize()
+    finally:
+        ipm.set_option("ragged_kernel", "auto")
+    for o in outs:
+        assert o.cpu().numpy().tobytes() == want.tobytes()
+
+
 def test_nondeterministic_mode_parity(ipm):
     ipm.set_option("deterministic", 0)
     try:
