@@ -313,14 +313,17 @@ struct Launch {
   }
   // marked rows (two passes, k_ragged_mark + k_ragged_mk, then the fix-up): chunks of 512 elements (4-byte) / 256
   // (8-byte), 8 CTAs x 4 warps per SM; the scratch (bitmap + chunk counts) is zeroed in stream order first
-  // widened folds (float32 + *: float64 accumulators) 4 vectors per lane at 6 CTAs per SM, the others 2 at 8; every
-  // fold asks L2 for the chunk after the next (profiles/r02_ab_marked_1.txt)
+  // shape per fold (same-box A/B, profiles/r02_ab_marked_{1,3,4}.txt): folds with 8-byte accumulators on 4-byte
+  // elements (float32 + * in float64, float32 max/min pairs) 4 vectors per lane at 6 CTAs per SM (shared memory
+  // bound); 8-byte compare / bitwise / logical folds 4 at 7 (+3..31 %); the rest (4-byte folds, 8-byte + *) 2 at 8;
+  // every fold asks L2 for the chunk after the next (profiles/r02_ab_marked_1.txt)
   static constexpr bool MK_WIDE = sizeof(typename R::A) > sizeof(typename R::B);
+  static constexpr bool MK_CMP8 = sizeof(typename R::B) == 8 && OP != IPM_ADD && OP != IPM_MUL;
 #ifndef IPM_MK_VPL
-#define IPM_MK_VPL (MK_WIDE ? 4 : 2)
+#define IPM_MK_VPL (MK_WIDE || MK_CMP8 ? 4 : 2)
 #endif
 #ifndef IPM_MK_MINB
-#define IPM_MK_MINB (MK_WIDE ? 6 : 8)
+#define IPM_MK_MINB (MK_WIDE ? 6 : MK_CMP8 ? 7 : 8)
 #endif
 #ifndef IPM_MK_PFD
 #define IPM_MK_PFD 1
