@@ -233,16 +233,26 @@ struct Launch {
     k_ragged_fix<R><<<(unsigned)((blocks + 7) / 8), 256, 0, st>>>(p, blocks);
     return cudaSuccess;
   }
+  // the warp kernel's shape: 2 vectors per lane at 8 CTAs x 4 warps per SM; 8-byte compare / bitwise / logical
+  // folds 4 vectors at IPM_RV_CMP8 = 6 CTAs (same-box A/B, profiles/r02_ab_ragged_vec_cmp8.txt: float64 max/min
+  // +25-29 %, int64 max +11-14 %, int64 && +8-11 %, 7 CTAs slightly slower; the float64 max/min instantiations keep
+  // a 4-byte spill outside the chunk loop, tests/test_build_report.py)
+  static constexpr bool RV_CMP8 = sizeof(typename R::B) == 8 && OP != IPM_ADD && OP != IPM_MUL;
+#ifndef IPM_RV_CMP8
+#define IPM_RV_CMP8 6
+#endif
+  static constexpr int RV_VPL = RV_CMP8 ? 4 : 2, RV_MINB = RV_CMP8 ? IPM_RV_CMP8 : 8;
+  static int64_t ragged_vec_warps(int sms) { return std::min<int64_t>((int64_t)sms * 4 * RV_MINB, WS_MAX_RAGGED_WARPS); }
   static void ragged_vec_only(const RaggedParams& p, int blocks, cudaStream_t st) {
     // 25 KiB of static shared memory per CTA: ask for the largest carveout so 8 CTAs fit on an SM
     // L2 prefetch of the next chunk (profiles/r01_sweep_ragged_5_l2prefetch.txt: +13-16 % on long rows, +1-7 % on
     // the power-law graph); for the widened float32 + * fold (issue-bound on short rows) only inside long rows
     constexpr int PFV = sizeof(typename R::A) > sizeof(typename R::B) ? -1 : 1;
-    static const bool carveout = cudaFuncSetAttribute(k_ragged_vec<R, 4, 8, 2, true, PFV>,
+    static const bool carveout = cudaFuncSetAttribute(k_ragged_vec<R, 4, RV_MINB, RV_VPL, true, PFV>,
                                                       cudaFuncAttributePreferredSharedMemoryCarveout,
                                                       (int)cudaSharedmemCarveoutMaxShared) == cudaSuccess;
     (void)carveout;
-    k_ragged_vec<R, 4, 8, 2, true, PFV><<<blocks, 128, 0, st>>>(p);  // 8 CTAs x 4 warps per SM, 2 vectors per lane
+    k_ragged_vec<R, 4, RV_MINB, RV_VPL, true, PFV><<<blocks, 128, 0, st>>>(p);  // RV_MINB CTAs x 4 warps per SM
   }
   static void ragged(const RaggedParams& p, int blocks, int64_t nw, cudaStream_t st) {
     ragged_vec_only(p, blocks, st);
@@ -302,13 +312,20 @@ struct Launch {
 #ifndef IPM_RA_LONG
 #define IPM_RA_LONG (sizeof(typename R::B) == 8 ? 128 : 256)
 #endif
-  static void ragged_auto(const RaggedParams& p0, int blocks, int64_t nw, cudaStream_t st) {
+  // each candidate on its own grid (the warp kernel: one wave of its shape; the lane-per-row kernel: 8 CTAs x 4
+  // warps per SM); the one that runs publishes its warp count (a workspace word) for the fix-up
+  static void ragged_auto(const RaggedParams& p0, int sms, cudaStream_t st) {
     RaggedParams p = p0;
+    p.nw_dev = (int64_t*)((char*)p.head_row - WS_RAGGED + WS_RAGGED_NW);
+    const int64_t nw_vec = ragged_vec_warps(sms);
+    const int64_t nw_lpr = std::min<int64_t>((int64_t)sms * 32, WS_MAX_RAGGED_WARPS);
     p.gate_len = IPM_RA_LONG;
     p.gate = 1;
-    ragged_vec_only(p, blocks, st);
+    ragged_vec_only(p, (int)(nw_vec / 4), st);
     p.gate = 2;
-    k_ragged_lpr<R, IPM_LP_WARPS, IPM_LP_MINB, IPM_LP_CAPB, 8, IPM_LP_T><<<blocks, IPM_LP_WARPS * 32, 0, st>>>(p);
+    k_ragged_lpr<R, IPM_LP_WARPS, IPM_LP_MINB, IPM_LP_CAPB, 8, IPM_LP_T>
+        <<<(unsigned)(nw_lpr / IPM_LP_WARPS), IPM_LP_WARPS * 32, 0, st>>>(p);
+    const int64_t nw = std::max(nw_vec, nw_lpr);
     k_ragged_fix<R><<<(unsigned)((nw + 7) / 8), 256, 0, st>>>(p, nw);
   }
   // marked rows (two passes, k_ragged_mark + k_ragged_mk, then the fix-up): chunks of 512 elements (4-byte) / 256
@@ -386,10 +403,11 @@ struct Table {
   cudaError_t (*ragged_tile)(const RaggedParams&, int, cudaStream_t);
   void (*ragged_rank)(const RaggedParams&, int, int64_t, cudaStream_t);
   void (*ragged_lpr)(const RaggedParams&, int, int64_t, cudaStream_t);
-  void (*ragged_auto)(const RaggedParams&, int, int64_t, cudaStream_t);
+  void (*ragged_auto)(const RaggedParams&, int, cudaStream_t);
   int (*ragged_rank_ctas_per_sm)();
   cudaError_t (*ragged_mk)(const RaggedParams&, const RaggedMarks&, size_t, int, int64_t, cudaStream_t);
   int64_t (*ragged_mk_warps)(int);
+  int64_t (*ragged_vec_warps)(int);
   void (*seg_warp)(const SegParams&, int, cudaStream_t);  // (params, SM count, stream)
   cudaError_t (*seg_tma)(const SegParams&, int, cudaStream_t);
   void (*seg_group)(const SegParams&, int, int, cudaStream_t);
@@ -400,7 +418,7 @@ struct Table {
 static const Table* table(ipm_op op, ipm_dtype dt) {
 #define IPM_ENTRY(O, D)                                                                                  \
   if (op == O && dt == D) {                                                                            \
-    static const Table t = {&Launch<O, D>::flat, &Launch<O, D>::two_d, &Launch<O, D>::ragged, &Launch<O, D>::ragged_tile, &Launch<O, D>::ragged_rank, &Launch<O, D>::ragged_lpr, &Launch<O, D>::ragged_auto, &Launch<O, D>::ragged_rank_ctas_per_sm, &Launch<O, D>::ragged_mk, &Launch<O, D>::ragged_mk_warps, &Launch<O, D>::seg_warp, &Launch<O, D>::seg_tma,     \
+    static const Table t = {&Launch<O, D>::flat, &Launch<O, D>::two_d, &Launch<O, D>::ragged, &Launch<O, D>::ragged_tile, &Launch<O, D>::ragged_rank, &Launch<O, D>::ragged_lpr, &Launch<O, D>::ragged_auto, &Launch<O, D>::ragged_rank_ctas_per_sm, &Launch<O, D>::ragged_mk, &Launch<O, D>::ragged_mk_warps, &Launch<O, D>::ragged_vec_warps, &Launch<O, D>::seg_warp, &Launch<O, D>::seg_tma,     \
                             &Launch<O, D>::seg_group, &Launch<O, D>::finalize, &Launch<O, D>::exchange};\
     return &t;                                                                                         \
   }
@@ -1045,10 +1063,12 @@ ipm_status ipm_reduce_ragged(ipm_op op, ipm_dtype dt, const void* dev, const int
   p.out = dev_out;
   p.gate = 0;
   p.gate_len = 0;
+  p.nw_dev = nullptr;
   const int kopt = g_opt_ragged_kernel.load(std::memory_order_relaxed);
   const int kern = kopt;  // 0 auto: the warp kernel or, for long rows, the lane-per-row kernel (gated on device)
   const Table* tb = table(op, dt);
-  const int64_t nw = kern <= 1 || kern == 4 ? std::min<int64_t>((int64_t)sm_count() * 32, WS_MAX_RAGGED_WARPS)  // 8 CTAs x 4 warps per SM
+  const int64_t nw = kern <= 1 ? tb->ragged_vec_warps(sm_count())  // one wave of the warp kernel's CTAs
+                     : kern == 4 ? std::min<int64_t>((int64_t)sm_count() * 32, WS_MAX_RAGGED_WARPS)  // 8 CTAs x 4 warps per SM
                      : kern == 3 ? (int64_t)std::min<int64_t>((int64_t)sm_count() * tb->ragged_rank_ctas_per_sm(),
                                                               WS_MAX_RAGGED_WARPS / IPM_RR_WARPS) *
                                            IPM_RR_WARPS  // one wave of CTAs
@@ -1061,7 +1081,7 @@ ipm_status ipm_reduce_ragged(ipm_op op, ipm_dtype dt, const void* dev, const int
   cudaStream_t st = (cudaStream_t)stream;
   {
     ProfScope ps(st, 4);
-    if (kern == 0) tb->ragged_auto(p, (int)(nw / 4), nw, st);
+    if (kern == 0) tb->ragged_auto(p, sm_count(), st);
     else if (kern == 1) tb->ragged(p, (int)(nw / 4), nw, st);
     else if (kern == 3) tb->ragged_rank(p, (int)(nw / IPM_RR_WARPS), nw, st);
     else if (kern == 4) tb->ragged_lpr(p, (int)(nw / IPM_LP_WARPS), nw, st);
@@ -1120,6 +1140,7 @@ ipm_status ipm_reduce_ragged_marked(ipm_op op, ipm_dtype dt, const void* dev, in
   p.out = dev_out;
   p.gate = 0;
   p.gate_len = 0;
+  p.nw_dev = nullptr;
   int64_t* base = (int64_t*)((char*)ws + WS_RAGGED);
   p.head_row = base;
   p.head_part = (uint64_t*)(base + WS_MAX_RAGGED_WARPS);

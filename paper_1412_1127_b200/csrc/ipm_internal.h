@@ -15,6 +15,7 @@ constexpr size_t WS_LOCAL = 4160;         // this rank's accumulator partial (mu
 constexpr size_t WS_ACC = 4224;           // running accumulator (host-streaming path)
 constexpr size_t WS_COUNTER = 4288;       // dynamic tile counter of the flat kernel (left at zero)
 constexpr size_t WS_PACKED = 4296;        // int32 + count-and-sum word of the static flat kernel (left at zero)
+constexpr size_t WS_RAGGED_NW = 4320;     // int64: warp count of the ragged kernel that ran (auto)
 constexpr size_t WS_SLOTS = 4352;         // gathered partials, one per rank
 constexpr int WS_MAX_RANKS = 64;
 constexpr size_t WS_PARTIALS = 8192;      // per-CTA partials

@@ -907,6 +907,8 @@ struct RaggedParams {
   uint64_t* tail_part;
   int gate;               // 0: run; 1: run only below gate_len elements per row on average; 2: only at or above
   int64_t gate_len;
+  int64_t* nw_dev;        // non-NULL (auto: gated candidates with different warp counts): the kernel that runs
+                          // stores its warp count here and the fix-up kernel scans only that many records
 };
 
 // first index r in [0, rows] with off[r] >= x (off non-decreasing); 32-ary search by the whole warp
@@ -972,6 +974,7 @@ __device__ __forceinline__ bool ragged_warp(RaggedWarp& g, const RaggedParams& p
   if ((threadIdx.x & 31) == 0) {
     p.head_row[w] = g.lo < g.hi ? -1 : -2;
     p.tail_row[w] = -1;
+    if (w == 0 && p.nw_dev) *p.nw_dev = nw;
   }
   return true;
 }
@@ -1237,6 +1240,7 @@ __global__ void __launch_bounds__(256) k_ragged_fix(RaggedParams p, int64_t nw) 
   using A = typename R::A;
   const int lane = threadIdx.x & 31;
   const int64_t w = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (p.nw_dev) nw = *(volatile int64_t*)p.nw_dev;  // auto: the warp count of the candidate that ran
   if (w >= nw) return;
   const int64_t row = p.tail_row[w];
   if (row < 0) return;

@@ -11,6 +11,11 @@ import pytest
 from tools import build
 
 HOT = ("k_flat_guided", "k_ragged_vec", "k_ragged_fix", "k_fused", "dist_exchange", "k_finalize")
+# measured exceptions: (demangled-name fragment, max spill store bytes, max spill load bytes, why)
+ALLOWED = [("k_ragged_vec<ipm::Red<2, 3>, 4, 6, 4,", 4, 8,
+            "float64 max: one STL before the row search, LDLs after it and at the end (cuobjdump), none in the "
+            "chunk loop; the 4-vector shape is 25-29 % faster (profiles/r02_ab_ragged_vec_cmp8.txt)"),
+           ("k_ragged_vec<ipm::Red<3, 3>, 4, 6, 4,", 4, 8, "float64 min: the same")]
 
 
 def _report():
@@ -38,6 +43,8 @@ def test_hot_kernels_do_not_spill():
     names = {k: (dem[i] if i < len(dem) and dem[i] else k) for i, k in enumerate(keys)}
     hot = {k: v for k, v in rep.items() if any(h in names[k] for h in HOT)}
     assert len([k for k in hot if "k_flat_guided" in names[k]]) == 30  # one per legal (op, dtype) pair
-    bad = {names[k]: v for k, v in hot.items() if v != (0, 0)}
+    def allowed(name, v):
+        return any(frag in name and v[0] <= st and v[1] <= ld for frag, st, ld, _ in ALLOWED)
+    bad = {names[k]: v for k, v in hot.items() if v != (0, 0) and not allowed(names[k], v)}
     assert not bad, bad
 
