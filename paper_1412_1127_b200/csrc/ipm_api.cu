@@ -233,15 +233,17 @@ struct Launch {
     k_ragged_fix<R><<<(unsigned)((blocks + 7) / 8), 256, 0, st>>>(p, blocks);
     return cudaSuccess;
   }
-  // the warp kernel's shape: 2 vectors per lane at 8 CTAs x 4 warps per SM; 8-byte compare / bitwise / logical
-  // folds 4 vectors at IPM_RV_CMP8 = 6 CTAs (same-box A/B, profiles/r02_ab_ragged_vec_cmp8.txt: float64 max/min
-  // +25-29 %, int64 max +11-14 %, int64 && +8-11 %, 7 CTAs slightly slower; the float64 max/min instantiations keep
-  // a 4-byte spill outside the chunk loop, tests/test_build_report.py)
-  static constexpr bool RV_CMP8 = sizeof(typename R::B) == 8 && OP != IPM_ADD && OP != IPM_MUL;
-#ifndef IPM_RV_CMP8
-#define IPM_RV_CMP8 6
+  // the warp kernel's shape: 2 vectors per lane at 8 CTAs x 4 warps per SM for 4-byte elements; 8-byte elements 4
+  // vectors at IPM_RV_8B = 6 CTAs (same-box A/B: compare / bitwise / logical folds profiles/r02_ab_ragged_vec_cmp8.txt,
+  // float64 max/min +25-29 %, int64 max +11-14 %, int64 && +8-11 %, 7 CTAs slightly slower; + and *
+  // profiles/r02_ab_ragged_vec_8b_add.txt, int64 + +6-9 %, float64 + * +1-6 %, -3..6 % on 4-element rows); 4-byte
+  // folds lose at 4 vectors (-2..16 %, profiles/r02_ab_ragged_vec_4b.txt). The float64 max/min instantiations keep a
+  // 4-byte spill outside the chunk loop (tests/test_build_report.py)
+#ifndef IPM_RV_8B
+#define IPM_RV_8B 6
 #endif
-  static constexpr int RV_VPL = RV_CMP8 ? 4 : 2, RV_MINB = RV_CMP8 ? IPM_RV_CMP8 : 8;
+  static constexpr bool RV_8B = sizeof(typename R::B) == 8;
+  static constexpr int RV_VPL = RV_8B ? 4 : 2, RV_MINB = RV_8B ? IPM_RV_8B : 8;
   static int64_t ragged_vec_warps(int sms) { return std::min<int64_t>((int64_t)sms * 4 * RV_MINB, WS_MAX_RAGGED_WARPS); }
   static void ragged_vec_only(const RaggedParams& p, int blocks, cudaStream_t st) {
     // 25 KiB of static shared memory per CTA: ask for the largest carveout so 8 CTAs fit on an SM
