@@ -1379,13 +1379,14 @@ __global__ void __launch_bounds__(256) k_ragged_mark(RaggedParams p, RaggedMarks
           const uint32_t e = u < 3 ? (uint32_t)sv[u + 1 < 4 ? u + 1 : 3] : (uint32_t)e3;
           const uint32_t dw = t >> 5, dc = (t + offc) >> LCH;
           IPM_BOUND(w0 + dw < m.nwords && c0 + dc < m.nchunks);
+          const bool okw = w0 + dw < m.nwords, okc = c0 + dc < m.nchunks;  // (offsets out of contract: no write)
           if (dw < 64) atomicOr(win + dw, 1u << (t & 31));
-          else atomicOr(m.bits + w0 + dw, 1u << (t & 31));
+          else if (okw) atomicOr(m.bits + w0 + dw, 1u << (t & 31));
           if (dc < 8) atomicAdd(cwin + dc, 1u);
-          else atomicAdd(m.cnt + c0 + dc, 1u);
+          else if (okc) atomicAdd(m.cnt + c0 + dc, 1u);
           if (e == (uint32_t)sv[u]) {
             ((B*)p.out)[b + 4 * lane + u] = empty_val;
-            atomicOr(m.cnt + c0 + dc, 0x80000000u);
+            if (okc) atomicOr(m.cnt + c0 + dc, 0x80000000u);
           }
         }
       }
@@ -1399,13 +1400,14 @@ __global__ void __launch_bounds__(256) k_ragged_mark(RaggedParams p, RaggedMarks
         const int64_t dw = (q >> 5) - w0, dc = (q >> LCH) - c0;
         const uint32_t bit = 1u << (q & 31);
         IPM_BOUND(q >= 0 && (q >> 5) < m.nwords && (q >> LCH) < m.nchunks && dw >= 0 && dc >= 0);
-        if (dw < 64) atomicOr(win + dw, bit);
-        else atomicOr(m.bits + (q >> 5), bit);
-        if (dc < 8) atomicAdd(cwin + dc, 1u);
-        else atomicAdd(m.cnt + (q >> LCH), 1u);
+        const bool okw = q >= 0 && (q >> 5) < m.nwords, okc = q >= 0 && (q >> LCH) < m.nchunks;
+        if (dw >= 0 && dw < 64) atomicOr(win + dw, bit);
+        else if (okw) atomicOr(m.bits + (q >> 5), bit);
+        if (dc >= 0 && dc < 8) atomicAdd(cwin + dc, 1u);
+        else if (okc) atomicAdd(m.cnt + (q >> LCH), 1u);
         if (e == sv[u]) {
           ((B*)p.out)[r] = empty_val;
-          atomicOr(m.cnt + (q >> LCH), 0x80000000u);
+          if (okc) atomicOr(m.cnt + (q >> LCH), 0x80000000u);
         }
       }
     }
@@ -1420,7 +1422,7 @@ __global__ void __launch_bounds__(256) k_ragged_mark(RaggedParams p, RaggedMarks
       const int dw = lane + 32 * h;
       const uint32_t word = win[dw];
       win[dw] = 0u;
-      if (word) {
+      if (word && w0 + dw < m.nwords) {
         IPM_BOUND(w0 + dw < m.nwords);
         if (dw == 0 || dw == dwl) atomicOr(m.bits + w0 + dw, word);
         else m.bits[w0 + dw] = word;
@@ -1429,7 +1431,7 @@ __global__ void __launch_bounds__(256) k_ragged_mark(RaggedParams p, RaggedMarks
     if (lane < 8) {
       const uint32_t c = cwin[lane];
       cwin[lane] = 0u;
-      if (c) {
+      if (c && c0 + lane < m.nchunks) {
         IPM_BOUND(c0 + lane < m.nchunks);
         atomicAdd(m.cnt + c0 + lane, c);
       }
@@ -1462,7 +1464,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_mk(RaggedParams p, 
   const B* a = (const B*)p.a;
   const int64_t P0 = __ldg(p.off), P1 = __ldg(p.off + p.rows);
   const int64_t G = ragged_origin<B>(p.a, P0);
-  const int64_t NC = P1 > P0 ? (P1 - G + CH - 1) / CH : 0;  // chunks holding elements
+  // chunks holding elements (bounded by the scratch: with off[rows] beyond the caller's nvalues — outside the
+  // contract — results are undefined but nothing outside the scratch is read)
+  const int64_t NC = min(P1 > P0 ? (P1 - G + CH - 1) / CH : 0, min(m.nchunks, m.nwords * 32 / CH));
   const int64_t c_lo = (int64_t)(((__int128)NC * w) / nw), c_hi = (int64_t)(((__int128)NC * (w + 1)) / nw);
   const int64_t lo = max(P0, G + c_lo * CH), hi = min(P1, G + c_hi * CH);
   if (lane == 0) {

@@ -484,6 +484,24 @@ def test_ragged_marked_side_stream(ipm):
         assert o.cpu().numpy().tobytes() == want.tobytes()
 
 
+def test_ragged_marked_offsets_beyond_nvalues_stay_in_scratch(ipm):
+    """Outside the contract (off[rows] > nvalues, the bound the scratch is sized from) the results are undefined,
+    but the two-pass kernels must not write past the scratch: canary bytes after it stay intact."""
+    L = ipm.lib
+    nvalues = 1000
+    x = torch.ones(1 << 20, dtype=torch.float32, device="cuda")  # the kernels may read past nvalues, not past x
+    off = torch.tensor([0, 10, 500_000, 900_000], dtype=torch.int64, device="cuda")
+    need = L.ipm_ragged_scratch_bytes(2, nvalues)
+    scratch = torch.full((need + 4096,), 0xAB, dtype=torch.uint8, device="cuda")
+    out = torch.zeros(3, dtype=torch.float32, device="cuda")
+    ws = ipm.workspace()
+    rc = L.ipm_reduce_ragged_marked(0, 2, x.data_ptr(), nvalues, off.data_ptr(), 3, None, out.data_ptr(),
+                                    ws.data_ptr(), scratch.data_ptr(), need, ipm._stream())
+    torch.cuda.synchronize()
+    assert rc == 0
+    assert bool((scratch[need:] == 0xAB).all())
+
+
 def test_nondeterministic_mode_parity(ipm):
     ipm.set_option("deterministic", 0)
     try:
