@@ -356,8 +356,19 @@ struct Launch {
                                cudaStream_t st) {
     cudaError_t e = cudaMemsetAsync(m.bits, 0, zero_bytes, st);
     if (e != cudaSuccess) return e;
-    const int64_t blocks0 = std::min<int64_t>((p.rows + 1023) / 1024, (int64_t)sms * 4);  // 8 warps x 128 rows; 4 CTAs per SM fit (58 registers)
-    k_ragged_mark<R, MK_CH><<<(unsigned)blocks0, 256, 0, st>>>(p, m);
+#ifndef IPM_MK_RPL
+#define IPM_MK_RPL 8
+#endif
+    // 8 warps x 32 x RPL rows per CTA step; one wave of the CTAs that fit (74 registers: 3 per SM at RPL 8). RPL 8
+    // against 4: power-law +2-3 %, uniform rows +2-4 %, 4-element rows +4-6 %, 64-element rows -1..4 %
+    // (profiles/r02_ab_mark_rpl.txt)
+    static const int occ0 = [] {
+      int n = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_ragged_mark<R, MK_CH, IPM_MK_RPL>, 256, 0);
+      return n > 0 ? n : 1;
+    }();
+    const int64_t blocks0 = std::min<int64_t>((p.rows + 256 * IPM_MK_RPL - 1) / (256 * IPM_MK_RPL), (int64_t)sms * occ0);
+    k_ragged_mark<R, MK_CH, IPM_MK_RPL><<<(unsigned)blocks0, 256, 0, st>>>(p, m);
     static const bool carveout = cudaFuncSetAttribute(k_ragged_mk<R, 4, MK_MINB, MK_VPL, MK_PFD>,
                                                       cudaFuncAttributePreferredSharedMemoryCarveout,
                                                       (int)cudaSharedmemCarveoutMaxShared) == cudaSuccess;

@@ -1308,117 +1308,126 @@ __device__ __forceinline__ int64_t ragged_origin(const void* a, int64_t P0) {
   return P0 - (int64_t)(((uintptr_t)((const B*)a + P0) & 31u) / sizeof(B));
 }
 
-// pass 0: 128 consecutive rows per warp step, 4 per lane (one 32-byte load of off[] per lane, the next step's
-// issued before this one is processed). The row starts' bits are OR-ed into a per-warp shared-memory window of
-// the 64 bitmap words from the step's first row, its row counts into a window of the 8 chunks from the first
-// row's chunk (shared atomics); a row beyond a window (rows longer than 16 elements on average) updates global
-// memory itself. Each non-zero word is then written once: plainly if only this step's rows can start in it
+// pass 0: 32 x RPL consecutive rows per warp step, RPL per lane (RPL / 4 32-byte loads of off[] per lane, the next
+// step's issued before this one is processed). The row starts' bits are OR-ed into a per-warp shared-memory window
+// of the 16 x RPL bitmap words from the step's first row, its row counts into a window of the 2 x RPL chunks from
+// the first row's chunk (shared atomics); a row beyond a window (rows longer than 16 elements on average) updates
+// global memory itself. Each non-zero word is then written once: plainly if only this step's rows can start in it
 // (strictly between its first and last row's words), atomically at the two ends (shared with the neighbouring
 // steps); chunk counts are added atomically. Empty rows: result written, chunk flagged (bit 31).
-template <class R, int CH>
+template <class R, int CH, int RPL = 4>
 __global__ void __launch_bounds__(256) k_ragged_mark(RaggedParams p, RaggedMarks m) {
   using B = typename R::B;
   static_assert((CH & (CH - 1)) == 0, "chunk: a power of two");
+  static_assert(RPL == 4 || RPL == 8, "rows per lane: one or two 32-byte loads");
   constexpr int LCH = __builtin_ctz(CH);
-  __shared__ uint32_t s_win[8][64];
-  __shared__ uint32_t s_cnt[8][8];
+  constexpr int STEP = 32 * RPL, WW = 16 * RPL, CW = 2 * RPL;
+  __shared__ uint32_t s_win[8][WW];
+  __shared__ uint32_t s_cnt[8][CW];
   const int lane = threadIdx.x & 31;
   uint32_t* win = s_win[threadIdx.x >> 5];
   uint32_t* cwin = s_cnt[threadIdx.x >> 5];
-  win[lane] = 0u;
-  win[lane + 32] = 0u;
-  if (lane < 8) cwin[lane] = 0u;
+#pragma unroll
+  for (int h = 0; h < WW / 32; ++h) win[lane + 32 * h] = 0u;
+  if (lane < CW) cwin[lane] = 0u;
   const int64_t rows = p.rows;
   const int64_t P0 = __ldg(p.off);
   const int64_t G = ragged_origin<B>(p.a, P0);
   const B empty_val = R::fin(p.has_init ? R::op(R::lift((B)p.init), R::id()) : R::id());
-  const int64_t stride = (int64_t)gridDim.x * 8 * 128;
+  const int64_t stride = (int64_t)gridDim.x * 8 * STEP;
   const bool vec = ((uintptr_t)p.off & 31u) == 0;  // 32-byte loads of 4 offsets
-  // off[b + 4 lane + u], u < 4 (clamped to off[rows])
-  auto load4 = [&](int64_t b, int64_t (&v)[4]) {
-    const int64_t r = b + 4 * lane;
-    if (vec && r + 3 < rows) {
-      const V4 t = ldv<1>((const V4*)(p.off + r));
+  // off[b + RPL lane + u], u < RPL (clamped to off[rows])
+  auto loadr = [&](int64_t b, int64_t (&v)[RPL]) {
+    const int64_t r = b + RPL * lane;
+    if (vec && r + RPL - 1 < rows) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = (int64_t)t.w[u];
+      for (int h = 0; h < RPL / 4; ++h) {
+        const V4 t = ldv<1>((const V4*)(p.off + r + 4 * h));
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[4 * h + u] = (int64_t)t.w[u];
+      }
     } else {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = __ldg(p.off + (r + u < rows ? r + u : rows));
+      for (int u = 0; u < RPL; ++u) v[u] = __ldg(p.off + (r + u < rows ? r + u : rows));
     }
   };
-  int64_t b = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * 128;
-  int64_t nx[4], nx_end = 0;  // the next step's offsets and the end of its last row, loaded a step ahead
+  int64_t b = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * STEP;
+  int64_t nx[RPL], nx_end = 0;  // the next step's offsets and the end of its last row, loaded a step ahead
   if (b < rows) {
-    load4(b, nx);
-    nx_end = __ldg(p.off + (b + 128 < rows ? b + 128 : rows));
+    loadr(b, nx);
+    nx_end = __ldg(p.off + (b + STEP < rows ? b + STEP : rows));
   }
   __syncwarp();
   for (; b < rows; b += stride) {
-    int64_t sv[4];
+    int64_t sv[RPL];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) sv[u] = nx[u];
-    const int64_t bend = b + 128 < rows ? b + 128 : rows;
+    for (int u = 0; u < RPL; ++u) sv[u] = nx[u];
+    const int64_t bend = b + STEP < rows ? b + STEP : rows;
     const int64_t s_end = nx_end;  // the end of the step's last row
     if (b + stride < rows) {
-      load4(b + stride, nx);
-      nx_end = __ldg(p.off + (b + stride + 128 < rows ? b + stride + 128 : rows));
+      loadr(b + stride, nx);
+      nx_end = __ldg(p.off + (b + stride + STEP < rows ? b + stride + STEP : rows));
     }
     const int64_t q0 = __shfl_sync(FULL, sv[0], 0) - G;  // the step's first row start, relative to G
     const int64_t w0 = q0 >> 5, c0 = q0 >> LCH;
     const int64_t nxt = __shfl_down_sync(FULL, sv[0], 1);
     const int64_t e3 = lane == 31 ? s_end : nxt;
-    const int nr = (int)(bend - b);                    // rows in this step (<= 128)
+    const int nr = (int)(bend - b);                    // rows in this step (<= STEP)
     const int64_t base = G + (w0 << 5);                // bit 0 of the window's first word
     if (s_end - base < ((int64_t)1 << 31)) {           // warp-uniform: the step spans < 2^31 elements: 32 bits
       const uint32_t offc = (uint32_t)((w0 << 5) - (c0 << LCH));
       const uint32_t blo = (uint32_t)base;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (4 * lane + u < nr) {
+      for (int u = 0; u < RPL; ++u) {
+        if (RPL * lane + u < nr) {
           const uint32_t t = (uint32_t)sv[u] - blo;  // position relative to the window's first word
-          const uint32_t e = u < 3 ? (uint32_t)sv[u + 1 < 4 ? u + 1 : 3] : (uint32_t)e3;
+          const uint32_t e = u < RPL - 1 ? (uint32_t)sv[u + 1 < RPL ? u + 1 : RPL - 1] : (uint32_t)e3;
           const uint32_t dw = t >> 5, dc = (t + offc) >> LCH;
           IPM_BOUND(w0 + dw < m.nwords && c0 + dc < m.nchunks);
           const bool okw = w0 + dw < m.nwords, okc = c0 + dc < m.nchunks;  // (offsets out of contract: no write)
-          if (dw < 64) atomicOr(win + dw, 1u << (t & 31));
+          if (dw < WW) atomicOr(win + dw, 1u << (t & 31));
           else if (okw) atomicOr(m.bits + w0 + dw, 1u << (t & 31));
-          if (dc < 8) atomicAdd(cwin + dc, 1u);
+          if (dc < CW) atomicAdd(cwin + dc, 1u);
           else if (okc) atomicAdd(m.cnt + c0 + dc, 1u);
           if (e == (uint32_t)sv[u]) {
-            ((B*)p.out)[b + 4 * lane + u] = empty_val;
+            ((B*)p.out)[b + RPL * lane + u] = empty_val;
             if (okc) atomicOr(m.cnt + c0 + dc, 0x80000000u);
           }
         }
       }
     } else {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int64_t r = b + 4 * lane + u;
-      if (r < rows) {
-        const int64_t q = sv[u] - G;
-        const int64_t e = u < 3 ? sv[u + 1 < 4 ? u + 1 : 3] : e3;
-        const int64_t dw = (q >> 5) - w0, dc = (q >> LCH) - c0;
-        const uint32_t bit = 1u << (q & 31);
-        IPM_BOUND(q >= 0 && (q >> 5) < m.nwords && (q >> LCH) < m.nchunks && dw >= 0 && dc >= 0);
-        const bool okw = q >= 0 && (q >> 5) < m.nwords, okc = q >= 0 && (q >> LCH) < m.nchunks;
-        if (dw >= 0 && dw < 64) atomicOr(win + dw, bit);
-        else if (okw) atomicOr(m.bits + (q >> 5), bit);
-        if (dc >= 0 && dc < 8) atomicAdd(cwin + dc, 1u);
-        else if (okc) atomicAdd(m.cnt + (q >> LCH), 1u);
-        if (e == sv[u]) {
-          ((B*)p.out)[r] = empty_val;
-          if (okc) atomicOr(m.cnt + (q >> LCH), 0x80000000u);
+      for (int u = 0; u < RPL; ++u) {
+        const int64_t r = b + RPL * lane + u;
+        if (r < rows) {
+          const int64_t q = sv[u] - G;
+          const int64_t e = u < RPL - 1 ? sv[u + 1 < RPL ? u + 1 : RPL - 1] : e3;
+          const int64_t dw = (q >> 5) - w0, dc = (q >> LCH) - c0;
+          const uint32_t bit = 1u << (q & 31);
+          IPM_BOUND(q >= 0 && (q >> 5) < m.nwords && (q >> LCH) < m.nchunks && dw >= 0 && dc >= 0);
+          const bool okw = q >= 0 && (q >> 5) < m.nwords, okc = q >= 0 && (q >> LCH) < m.nchunks;
+          if (dw >= 0 && dw < WW) atomicOr(win + dw, bit);
+          else if (okw) atomicOr(m.bits + (q >> 5), bit);
+          if (dc >= 0 && dc < CW) atomicAdd(cwin + dc, 1u);
+          else if (okc) atomicAdd(m.cnt + (q >> LCH), 1u);
+          if (e == sv[u]) {
+            ((B*)p.out)[r] = empty_val;
+            if (okc) atomicOr(m.cnt + (q >> LCH), 0x80000000u);
+          }
         }
       }
     }
-    }
     // the step's last row's word, relative to w0
-    const int lastl = (int)((bend - 1 - b) >> 2), lastu = (int)((bend - 1 - b) & 3);
-    const int64_t sl = __shfl_sync(FULL, lastu == 0 ? sv[0] : lastu == 1 ? sv[1] : lastu == 2 ? sv[2] : sv[3], lastl);
+    const int lastl = (nr - 1) / RPL, lastu = (nr - 1) % RPL;
+    int64_t pick = sv[0];
+#pragma unroll
+    for (int u = 1; u < RPL; ++u)
+      if (u == lastu) pick = sv[u];
+    const int64_t sl = __shfl_sync(FULL, pick, lastl);
     const int64_t dwl = ((sl - G) >> 5) - w0;
     __syncwarp();
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < WW / 32; ++h) {
       const int dw = lane + 32 * h;
       const uint32_t word = win[dw];
       win[dw] = 0u;
@@ -1428,7 +1437,7 @@ __global__ void __launch_bounds__(256) k_ragged_mark(RaggedParams p, RaggedMarks
         else m.bits[w0 + dw] = word;
       }
     }
-    if (lane < 8) {
+    if (lane < CW) {
       const uint32_t c = cwin[lane];
       cwin[lane] = 0u;
       if (c && c0 + lane < m.nchunks) {
