@@ -259,7 +259,9 @@ typedef enum {
                                    3 one warp per element range, rows finished in row order (k_ragged_rank),
                                    4 one warp per element range, lane per row over shared-memory windows
                                      (k_ragged_lpr). Measured on one B200: 1 the fastest on
-                                     rows of tens of elements, 3 on short power-law rows, 4 on rows of >= 256. */
+                                     rows of tens of elements, 3 on short power-law rows, 4 on rows of >= 256.
+                                   The two-pass form is a separate entry point, ipm_reduce_ragged_marked (the
+                                   fastest on short power-law rows; this option does not apply to it). */
 } ipm_option;
 ipm_status ipm_set_option(ipm_option key, int64_t value);
 

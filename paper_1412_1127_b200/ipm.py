@@ -484,7 +484,8 @@ SEG_KERNELS = {"auto": 0, "warp": 1, "ldg": 1, "tma": 2}
 
 def set_option(key: str, value) -> None:
     """Process-wide tuning option (ipm_set_option): flat_ctas_per_sm (1..8, -1 default), seg_kernel
-    ('auto' | 'warp' | 'tma')."""
+    ('auto' | 'warp' | 'tma'), ragged_kernel ('auto' | 'warp' | 'tile' | 'rank' | 'lpr', or 'marked': reduce_ragged
+    then calls ipm_reduce_ragged_marked with scratch from torch's caching allocator)."""
     if key == "seg_kernel" and isinstance(value, str):
         value = SEG_KERNELS[value]
     if key == "dist_mode" and isinstance(value, str):
