@@ -201,11 +201,11 @@ ipm_status ipm_reduce_ragged(ipm_op op, ipm_dtype dt, const void* dev, const int
  * element-parallel pass then folds the elements, reading each lane's row-start flags from the bitmap and naming
  * rows by rank within their chunk instead of walking the row offsets per chunk.
  * nvalues: the element array's length, >= off[rows] (the bound the scratch is sized from).
- * scratch: 256-byte aligned device buffer of at least ipm_ragged_scratch_bytes(dt, nvalues) bytes, caller-owned;
+ * scratch: 256-byte aligned device buffer of at least ipm_ragged_scratch_bytes(dt, nvalues, rows) bytes, caller-owned;
  *   its contents on entry do not matter (the library zeroes it in stream order); not used after the call's
  *   kernels complete. Too small -> IPM_E_WORKSPACE; misaligned -> IPM_E_ALIGN.
  * Four launches on `stream` (memset, mark, fold, fix-up); workspace as for ipm_reduce_ragged. */
-size_t ipm_ragged_scratch_bytes(ipm_dtype dt, int64_t nvalues);
+size_t ipm_ragged_scratch_bytes(ipm_dtype dt, int64_t nvalues, int64_t rows);
 ipm_status ipm_reduce_ragged_marked(ipm_op op, ipm_dtype dt, const void* dev, int64_t nvalues,
                                     const int64_t* dev_offsets, int64_t rows, const void* init, void* dev_out,
                                     void* workspace, void* scratch, size_t scratch_bytes, void* stream);

@@ -1112,9 +1112,10 @@ static size_t rmk_cnt_bytes(ipm_dtype dt, int64_t nvalues) {
   const int64_t ch = 32 * 32 / (int64_t)esize(dt) * 2;  // the marked kernel's smallest chunk (2 vectors per lane)
   return (((size_t)((nvalues + 64) / ch + 2)) * 4 + 255) & ~(size_t)255;
 }
-size_t ipm_ragged_scratch_bytes(ipm_dtype dt, int64_t nvalues) {
-  if (nvalues < 0 || esize(dt) == 0) return 0;
-  return rmk_bits_bytes(nvalues) + rmk_cnt_bytes(dt, nvalues);
+static size_t rmk_ebits_bytes(int64_t rows) { return (((size_t)(rows + 31) / 32 + 1) * 4 + 255) & ~(size_t)255; }
+size_t ipm_ragged_scratch_bytes(ipm_dtype dt, int64_t nvalues, int64_t rows) {
+  if (nvalues < 0 || rows < 0 || esize(dt) == 0) return 0;
+  return rmk_bits_bytes(nvalues) + rmk_cnt_bytes(dt, nvalues) + rmk_ebits_bytes(rows);
 }
 
 ipm_status ipm_reduce_ragged_marked(ipm_op op, ipm_dtype dt, const void* dev, int64_t nvalues,
@@ -1140,8 +1141,8 @@ ipm_status ipm_reduce_ragged_marked(ipm_op op, ipm_dtype dt, const void* dev, in
     set_error("device pointer not aligned to its element size (scratch: 256 bytes)");
     return IPM_E_ALIGN;
   }
-  if (scratch_bytes < ipm_ragged_scratch_bytes(dt, nvalues)) {
-    set_error("ragged scratch smaller than ipm_ragged_scratch_bytes(dt, nvalues)");
+  if (scratch_bytes < ipm_ragged_scratch_bytes(dt, nvalues, rows)) {
+    set_error("ragged scratch smaller than ipm_ragged_scratch_bytes(dt, nvalues, rows)");
     return IPM_E_WORKSPACE;
   }
   RaggedParams p;
@@ -1164,12 +1165,14 @@ ipm_status ipm_reduce_ragged_marked(ipm_op op, ipm_dtype dt, const void* dev, in
   m.cnt = (uint32_t*)((char*)scratch + rmk_bits_bytes(nvalues));
   m.nwords = (int64_t)(rmk_bits_bytes(nvalues) / 4);
   m.nchunks = (int64_t)(rmk_cnt_bytes(dt, nvalues) / 4);
+  m.ebits = (uint32_t*)((char*)m.cnt + rmk_cnt_bytes(dt, nvalues));
+  m.newords = (int64_t)(rmk_ebits_bytes(rows) / 4);
   const Table* tb = table(op, dt);
   const int64_t nw = tb->ragged_mk_warps(sm_count());
   cudaStream_t st = (cudaStream_t)stream;
   {
     ProfScope ps(st, 4);
-    CK(tb->ragged_mk(p, m, ipm_ragged_scratch_bytes(dt, nvalues), sm_count(), nw, st));
+    CK(tb->ragged_mk(p, m, rmk_bits_bytes(nvalues) + rmk_cnt_bytes(dt, nvalues), sm_count(), nw, st));
   }
   CK(cudaGetLastError());
   return IPM_OK;

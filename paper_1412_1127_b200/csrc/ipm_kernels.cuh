@@ -1281,14 +1281,17 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 //  pass 1 (k_ragged_mk, element-parallel): warp w owns whole chunks; per chunk each lane reads its EPL flag bits
 //    from the bitmap (one 32-bit load), folds its elements with parking exactly as k_ragged_vec, and names rows by
 //    RANK: the k-th flagged position of the chunk starts row R + k, R = rows started before the chunk (a running
-//    sum of cnt). In a chunk that holds an empty row (cnt bit 31) a flag's row is found by a binary search of the
-//    chunk's rows (the last row starting at or before the flag). Rows crossing warps: head / tail records and
-//    k_ragged_fix as for the other kernels.
+//    sum of cnt). In a chunk that holds an empty row (cnt bit 31) a flag's row is the (rank+1)-th non-empty row from
+//    the chunk's first row: a clear bit of the empty-row bitmap the row pass also writes (2-3 words prefetched a chunk
+//    ahead; a binary search beyond them). Rows crossing warps: head / tail records and k_ragged_fix as for the
+//    other kernels.
 // Scratch (caller-owned, ipm_ragged_scratch_bytes): the bitmap and the chunk counts, zeroed by the launcher.
 struct RaggedMarks {
   uint32_t* bits;  // bit q = some row starts at element G + q
   uint32_t* cnt;   // per chunk: rows starting in it (bits 0..30), one of them empty (bit 31)
   int64_t nwords, nchunks;  // their sizes (checked in the IPM_CHECK_BOUNDS build)
+  uint32_t* ebits;  // bit r = row r is empty (every word written by the row pass: no zeroing needed)
+  int64_t newords;
 };
 // IPM_CHECK_BOUNDS (a test build, tools/gpu_bounds.sh; compute-sanitizer is not available on the GPU pool): every
 // scratch, output and offsets index of the marked kernels is checked and a violation traps
@@ -1373,6 +1376,22 @@ __global__ void __launch_bounds__(256) k_ragged_mark(RaggedParams p, RaggedMarks
     const int64_t nxt = __shfl_down_sync(FULL, sv[0], 1);
     const int64_t e3 = lane == 31 ? s_end : nxt;
     const int nr = (int)(bend - b);                    // rows in this step (<= STEP)
+    // the empty-row words of this step (b is a multiple of STEP): lane l holds the bits of rows b + RPL l + u
+    {
+      uint32_t em = 0u;
+#pragma unroll
+      for (int u = 0; u < RPL; ++u) {
+        const int64_t e = u < RPL - 1 ? sv[u + 1 < RPL ? u + 1 : RPL - 1] : e3;
+        if (RPL * lane + u < nr && e == sv[u]) em |= 1u << u;
+      }
+#pragma unroll
+      for (int j = 1; j < 32 / RPL; ++j) {
+        const uint32_t o = __shfl_down_sync(FULL, em, j);
+        if ((lane & (32 / RPL - 1)) == 0) em |= o << (RPL * j);
+      }
+      const int64_t ew = (b >> 5) + lane / (32 / RPL);
+      if ((lane & (32 / RPL - 1)) == 0 && ew < m.newords) m.ebits[ew] = em;
+    }
     const int64_t base = G + (w0 << 5);                // bit 0 of the window's first word
     if (s_end - base < ((int64_t)1 << 31)) {           // warp-uniform: the step spans < 2^31 elements: 32 bits
       const uint32_t offc = (uint32_t)((w0 << 5) - (c0 << LCH));
@@ -1458,17 +1477,18 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_mk(RaggedParams p, 
   constexpr int EPL = VW * VPL;  // elements per lane per chunk: 16 (4-byte) / 8 (8-byte) flag bits
   constexpr int CH = 32 * EPL;
   static_assert(EPL == 32 || EPL == 16 || EPL == 8, "a lane's flags are a 32-, 16- or 8-bit field of one bitmap word");
-  // per warp, column-major by lane: the value of the segment that ends just before a flagged position; and, in a
-  // chunk that holds an empty row, the row of each of the first RMAP flags (by rank)
-  constexpr int RMAP = 64;
+  // per warp, column-major by lane: the value of the segment that ends just before a flagged position
   __shared__ A s_val[WARPS][CH];
-  __shared__ int s_rmap[WARPS][RMAP];
-  __shared__ int64_t s_offn[WARPS][RMAP + 1];  // the next chunk's first RMAP + 1 offsets (cp.async, if it has empties)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   A* const val_col = s_val[wid] + lane;
-  int* const rmap = s_rmap[wid];
-  int64_t* const offn = s_offn[wid];
-  bool pf_ready = false;  // warp-uniform: offn holds the current chunk's offsets
+  // a chunk holding an empty row names a flag's row from the empty-row bitmap: the first EW words from the chunk's
+  // first row, loaded at the end of the previous chunk (its count word, which says whether it has empties, arrived
+  // a chunk ahead)
+  constexpr int EW = CH >= 1024 ? 3 : 2;  // words: the chunk's rows at >= 16 elements per row on average, + 1
+  uint32_t ew[EW];
+#pragma unroll
+  for (int i = 0; i < EW; ++i) ew[i] = 0u;
+  bool ew_ready = false;  // warp-uniform: ew holds the current chunk's words
   const int64_t w = (int64_t)blockIdx.x * WARPS + wid, nw = (int64_t)gridDim.x * WARPS;
   const B* a = (const B*)p.a;
   const int64_t P0 = __ldg(p.off), P1 = __ldg(p.off + p.rows);
@@ -1491,15 +1511,13 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_mk(RaggedParams p, 
     IPM_BOUND(row >= 0 && row < p.rows);
     ((B*)p.out)[row] = R::fin(has_init ? R::op(ia, v) : v);
   };
-  // copy off[R0n .. R0n + min(cnt, RMAP)] of chunk c + 1 into offn if that chunk holds an empty row
-  auto prefetch_offsets = [&](int64_t c, int64_t R0n, uint32_t cwn) -> bool {
-    if (c + 1 >= c_hi || !(cwn >> 31)) return false;
-    const int64_t lim = min((int64_t)(cwn & 0x7fffffffu), (int64_t)RMAP);
+  // the EW empty-row words from row R0x's word on (past the bitmap: all empty, never selected)
+  auto load_ew = [&](int64_t R0x) {
 #pragma unroll
-    for (int i = lane; i <= RMAP; i += 32)
-      if (i <= lim && R0n + i <= p.rows) cp_async8(offn + i, p.off + R0n + i);
-    cp_async_commit();
-    return true;
+    for (int i = 0; i < EW; ++i) {
+      const int64_t wi = (R0x >> 5) + i;
+      ew[i] = wi < m.newords ? __ldg(m.ebits + wi) : ~0u;
+    }
   };
   const unsigned lanemask_lt = (1u << lane) - 1u;
   constexpr unsigned FMASK = EPL == 32 ? 0xffffffffu : (1u << EPL) - 1u;
@@ -1567,9 +1585,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_mk(RaggedParams p, 
         }
       }
       open_val = R::op(open_val, R::warp(v));
-      if (pf_ready) cp_async_wait<0>();  // (unused: no flags) nothing may land after the buffer is reused
-      pf_ready = prefetch_offsets(c, R0 + (cw & 0x7fffffffu), cw_n);
       R0 += cw & 0x7fffffffu;
+      ew_ready = c + 1 < c_hi && (cw_n >> 31);
+      if (ew_ready) load_ew(R0);
       continue;
     }
     // lane-local segmented fold, one pass, parking at every flag (as k_ragged_vec)
@@ -1602,37 +1620,20 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_mk(RaggedParams p, 
     pre -= nf;
     const bool has_empty = (cw >> 31) != 0u;  // warp-uniform
     const int64_t cnt_c = cw & 0x7fffffffu;
-    if (has_empty) {  // rank -> row of the chunk's non-empty rows, for the first RMAP ranks (one pass over them)
-      if (pf_ready) {
-        cp_async_wait<0>();
-        __syncwarp();
-      }
-      int base = 0;
-      for (int64_t j0 = 0; j0 < cnt_c && base < RMAP; j0 += 32) {
-        const int64_t j = j0 + lane;
-        const bool in = j < cnt_c;
-        const bool sm = pf_ready && j < RMAP;  // warp-uniform per window (RMAP is a multiple of 32)
-        const int64_t st = !in ? 0 : sm ? offn[j] : __ldg(p.off + R0 + j);
-        const int64_t en = !in ? 0 : sm ? offn[j + 1] : __ldg(p.off + R0 + j + 1);
-        const unsigned ne = __ballot_sync(FULL, in && en > st);
-        const int rk = base + __popc(ne & lanemask_lt);
-        IPM_BOUND(!in || R0 + j + 1 <= p.rows);
-        if (((ne >> lane) & 1u) && rk < RMAP) rmap[rk] = (int)(j);
-        base += __popc(ne);
-      }
-      __syncwarp();
-    } else if (pf_ready) {
-      cp_async_wait<0>();
-      __syncwarp();
-    }
-    // the next chunk's offsets, if it holds an empty row (its count word arrived a chunk ago): copied now, read
-    // when that chunk builds its rank map
-    pf_ready = prefetch_offsets(c, R0 + cnt_c, cw_n);
-    // the row that starts at the lane's flag k (k-th bit): by rank, or (a chunk with an empty row) from the map,
-    // beyond it the last of the chunk's rows that starts at or before the position
+    if (has_empty && !ew_ready) load_ew(R0);  // (the warp's first chunk)
+    // the row that starts at the lane's flag k (k-th bit): by rank, or (a chunk with an empty row) the (rank+1)-th
+    // non-empty row from R0 — the (rank+1)-th clear bit of the empty-row words — and beyond those EW words the last of
+    // the chunk's rows that starts at or before the position (binary search)
     auto rid_of = [&](int k, int rank) -> int64_t {
       if (!has_empty) return R0 + rank;
-      if (rank < RMAP) return R0 + rmap[rank];
+      int kk = rank;
+#pragma unroll
+      for (int i = 0; i < EW; ++i) {
+        const uint32_t z = ~ew[i] & (i == 0 ? ~0u << (R0 & 31) : ~0u);
+        const int cz = __popc(z);
+        if (kk < cz) return (((R0 >> 5) + i) << 5) + (int64_t)__fns(z, 0, kk + 1);
+        kk -= cz;
+      }
       const int64_t pos = Bc + EPL * lane + k;
       int64_t l = R0, h = R0 + cnt_c - 1;
       while (l < h) {
@@ -1685,6 +1686,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_ragged_mk(RaggedParams p, 
     open_val = shfl_acc(sv, 31);
     open_rid = __shfl_sync(FULL, my_rid, 31 - __clz(bal));
     R0 += cnt_c;
+    ew_ready = c + 1 < c_hi && (cw_n >> 31);
+    if (ew_ready) load_ew(R0);
     __syncwarp();
   }
   // the row still open at hi

@@ -60,7 +60,7 @@ def _load():
         "ipm_reduce_async": ([ci, ci, vp, i64, vp, vp, vp, vp], ci),
         "ipm_reduce_segmented": ([ci, ci, vp, i64, i64, i64, vp, vp, vp, vp], ci),
         "ipm_reduce_ragged": ([ci, ci, vp, vp, i64, vp, vp, vp, vp], ci),
-        "ipm_ragged_scratch_bytes": ([ci, i64], sz),
+        "ipm_ragged_scratch_bytes": ([ci, i64, i64], sz),
         "ipm_reduce_ragged_marked": ([ci, ci, vp, i64, vp, i64, vp, vp, vp, vp, sz, vp], ci),
         "ipm_reduce_partials": ([ci, ci, vp, i64, vp, ci, ctypes.POINTER(ci), vp], ci),
         "ipm_finalize_partials": ([ci, ci, vp, ci, vp, vp, vp], ci),
@@ -322,7 +322,8 @@ def reduce_ragged(op: str, values: torch.Tensor, offsets: torch.Tensor, init=Non
     box = _scalar(dt, init)
     if _ragged_marked[0]:  # two passes over scratch from torch's caching allocator (ipm_reduce_ragged_marked)
         nvalues = values.numel()
-        scratch = torch.empty(lib.ipm_ragged_scratch_bytes(dt, nvalues), dtype=torch.uint8, device=values.device)
+        scratch = torch.empty(lib.ipm_ragged_scratch_bytes(dt, nvalues, rows), dtype=torch.uint8,
+                              device=values.device)
         s = _stream(stream)
         _check(lib.ipm_reduce_ragged_marked(op_code(op), dt, ptr, nvalues, offsets.data_ptr(), rows,
                                             None if box is None else box.ctypes.data, out.data_ptr(), ws.data_ptr(),

@@ -82,9 +82,10 @@ def test_validation_before_cuda(ipm):
     assert "illegal" in L.ipm_last_error_message().decode() or L.ipm_last_error_message()
     # marked ragged rows: scratch size from the element count (bitmap bit per element + a count per chunk)
     offs, scr = ctypes.c_void_p(0x40000), ctypes.c_void_p(0x50000)
-    need = L.ipm_ragged_scratch_bytes(2, 1 << 20)
+    need = L.ipm_ragged_scratch_bytes(2, 1 << 20, 100)
     assert (1 << 20) // 8 < need <= (1 << 20) // 8 + (1 << 20) // 256 * 4 + 1024
-    assert need % 256 == 0 and L.ipm_ragged_scratch_bytes(3, 1 << 20) > need  # 8-byte types: half-size chunks
+    assert need % 256 == 0 and L.ipm_ragged_scratch_bytes(3, 1 << 20, 100) > need  # 8-byte types: half-size chunks
+    assert L.ipm_ragged_scratch_bytes(2, 1 << 20, 1 << 20) >= need + (1 << 20) // 8  # + a bit per row
     assert L.ipm_reduce_ragged_marked(0, 2, dev, 1 << 20, offs, 100, None, out, ws, scr, need - 256, None) == 7
     assert L.ipm_reduce_ragged_marked(0, 2, dev, 1 << 20, offs, 100, None, out, ws, ctypes.c_void_p(0x50010),
                                       need, None) == 6                        # scratch alignment

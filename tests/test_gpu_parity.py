@@ -475,7 +475,8 @@ def test_ragged_marked_side_stream(ipm):
             o = torch.empty(off.size - 1, dtype=torch.int32, device="cuda")
             o.record_stream(side)
             outs.append(ipm.reduce_ragged("^", x, offs, out=o, stream=side))
-            junk = torch.empty(ipm.lib.ipm_ragged_scratch_bytes(0, x.numel()), dtype=torch.uint8, device="cuda")
+            junk = torch.empty(ipm.lib.ipm_ragged_scratch_bytes(0, x.numel(), off.size - 1), dtype=torch.uint8,
+                               device="cuda")
             junk.fill_(0xFF)  # on the current stream, while the side stream may still be running
         side.synchronize()
     finally:
@@ -491,7 +492,7 @@ def test_ragged_marked_offsets_beyond_nvalues_stay_in_scratch(ipm):
     nvalues = 1000
     x = torch.ones(1 << 20, dtype=torch.float32, device="cuda")  # the kernels may read past nvalues, not past x
     off = torch.tensor([0, 10, 500_000, 900_000], dtype=torch.int64, device="cuda")
-    need = L.ipm_ragged_scratch_bytes(2, nvalues)
+    need = L.ipm_ragged_scratch_bytes(2, nvalues, 3)
     scratch = torch.full((need + 4096,), 0xAB, dtype=torch.uint8, device="cuda")
     out = torch.zeros(3, dtype=torch.float32, device="cuda")
     ws = ipm.workspace()
