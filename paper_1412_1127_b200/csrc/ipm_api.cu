@@ -242,8 +242,11 @@ struct Launch {
 #ifndef IPM_RV_8B
 #define IPM_RV_8B 6
 #endif
+#ifndef IPM_RV_4B
+#define IPM_RV_4B 8
+#endif
   static constexpr bool RV_8B = sizeof(typename R::B) == 8;
-  static constexpr int RV_VPL = RV_8B ? 4 : 2, RV_MINB = RV_8B ? IPM_RV_8B : 8;
+  static constexpr int RV_VPL = RV_8B ? 4 : 2, RV_MINB = RV_8B ? IPM_RV_8B : IPM_RV_4B;
   static int64_t ragged_vec_warps(int sms) { return std::min<int64_t>((int64_t)sms * 4 * RV_MINB, WS_MAX_RAGGED_WARPS); }
   static void ragged_vec_only(const RaggedParams& p, int blocks, cudaStream_t st) {
     // 25 KiB of static shared memory per CTA: ask for the largest carveout so 8 CTAs fit on an SM
